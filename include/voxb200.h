@@ -1,0 +1,218 @@
+/*
+ * voxb200.h — C-ABI of libvoxb200.so, the B200 (sm_100a) implementation of
+ * the arXiv 1807.03119 hot path: volume load -> Otsu histogram/threshold ->
+ * first-hit ray cast with the per-hit local noise filter (and the four
+ * comparison filters), Sobel normal, Phong shading -> image entropy.
+ *
+ * The reference (`voxray`, /root/reference/pkg/src/voxray) is pure Python;
+ * it has no FFI.  Its operator API is the Python module surface
+ * (pkg/src/voxray/__init__.py:3-43).  Each entry point below names the
+ * reference function it replaces; the Python mirror in
+ * paper_1807_03119_b200/ binds them with ctypes.
+ *
+ * Conventions
+ *  - every function returns an int status (VX_OK = 0); on failure
+ *    vx_last_error() returns a thread-local message.
+ *  - plain pointers and sizes only; "host" pointers are CPU memory, "dev"
+ *    pointers are CUDA device memory of the current device.
+ *  - the library is re-entrant: each calling thread gets its own CUDA stream;
+ *    the only shared mutable state is per-volume caches (mutex protected).
+ *  - volume layout: voxel (x, y, z) of an (nx, ny, nz) volume, x fastest,
+ *    exactly the reference's `Volume.data[z, y, x]` (volume.py:3-5).
+ */
+#ifndef VOXB200_H
+#define VOXB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum vx_status {
+  VX_OK = 0,
+  VX_EINVAL = 1, /* bad argument (maps to the reference's *Error classes) */
+  VX_ENOMEM = 2, /* device allocation failed                              */
+  VX_ECUDA = 3,  /* CUDA runtime error                                    */
+  VX_ERANGE = 5  /* value outside the exact-arithmetic range              */
+};
+
+/* FilterKind (filters.py:43-57), same order as the reference enum */
+enum vx_filter_kind {
+  VX_FILTER_NONE = 0,
+  VX_FILTER_MEAN = 1,
+  VX_FILTER_SIGMA = 2,
+  VX_FILTER_OKADA = 3,
+  VX_FILTER_ENTROPY = 4,
+  VX_FILTER_LOCAL_CLUSTER = 5,
+  /* vx_filter_batch only: axis_cluster_average_batch (filters.py:177-178) */
+  VX_FILTER_AXIS_CLUSTER = 6
+};
+
+typedef struct vx_volume vx_volume; /* opaque device replica of a Volume */
+
+/* Host-computed camera constants (render.py:188-201): the shim passes the
+ * exact FP64 values numpy computes in Camera.basis() (render.py:49-62). */
+typedef struct {
+  double right[3], up[3], fwd[3];
+  double origin[3]; /* Camera.position */
+  double tan_f;     /* math.tan(math.radians(fov_y_deg) / 2.0)  render.py:191 */
+  double aspect;    /* width / height                           render.py:192 */
+  int32_t width, height;
+} vx_ray_setup;
+
+/* March + shading constants (render.py:108-150, 258-290, 385-403). */
+typedef struct {
+  double step_size; /* RenderParams.step_size                              */
+  int32_t max_steps; /* > 0: explicit cap (RenderParams.max_steps); <= 0: derive
+                        from the longest span exactly as render.py:469-473  */
+  int32_t chunk;     /* max(1, min(16, int(15/step))) if step < 15 else 1    */
+  int32_t need_clip; /* chunk * step > 15  (render.py:286-287)               */
+  int32_t skip;      /* 1: exact empty-space skipping (default), 0: off      */
+  double ambient, diffuse, specular, shininess;
+  double light[3];   /* normalised light direction (render.py:512-513)      */
+  int32_t background;
+  int32_t _pad;
+} vx_render_params;
+
+/* Resolved FilterConfig (filters.py:60-126) plus the host statistics the
+ * filters need (histogram.py:109-116, filters.py:212-218). */
+typedef struct {
+  int32_t kind;           /* vx_filter_kind                                  */
+  int32_t kernel_size;    /* M, odd >= 3                                     */
+  int32_t cluster_offset; /* d >= 1                                          */
+  int32_t entropy_pairwise; /* vx_filter_batch only: 1 = numpy's 8-way pairwise
+                               order (the reference's single-coordinate batch) */
+  double threshold;       /* resolved T (float)                              */
+  double sigma_band;      /* sigma_mult * global_sigma (FP64, host)          */
+  double okada_threshold; /* T_d                                             */
+  double entropy_threshold; /* T_e                                           */
+  double entropy_lut[256];  /* entropy_terms(probabilities)                  */
+} vx_filter_config;
+
+/* Sort-first image partition for multi-GPU (tiles of 8x16 pixels dealt
+ * round-robin: tile t belongs to rank t % world). world = 1: whole frame. */
+typedef struct {
+  int32_t rank, world;
+} vx_partition;
+
+/* Render outputs.  Host variants: host pointers; *_device variants: device
+ * pointers.  Every pointer except pixels is nullable. */
+typedef struct {
+  uint8_t* pixels;       /* height*width, row-major from the top-left      */
+  int32_t* hit_voxel;    /* height*width*3 (x,y,z), -1 on miss              */
+  float* hit_t;          /* height*width, sample t of the accepted hit      */
+  double* hit_value;     /* height*width, filter value at the hit          */
+  double* intensity;     /* height*width, pre-quantisation Phong I          */
+  uint64_t* image_hist;  /* [256] grey-level histogram of pixels (fused K6) */
+  uint64_t* hit_count;   /* [1]                                             */
+  uint64_t* samples;     /* [1] march samples taken (diagnostic)            */
+  int32_t* trunc_flag;   /* [1] set to 1 when a ray exhausted its own
+                            span-derived step budget max(1, ceil(span/step)+1)
+                            without ending; only then can the frame-wide
+                            max_steps of render.py:469-473 differ from it.
+                            The host variant re-renders with the exact frame
+                            budget in that case; device callers must check.   */
+} vx_render_out;
+
+/* ---- device / errors ---------------------------------------------------- */
+const char* vx_last_error(void);
+int vx_version(void);
+int vx_device_count(int* n_out);
+int vx_set_device(int device);
+int vx_synchronize(void);
+
+/* ---- volume (volume.py:34-82, 122-151; grid.py:22-31) -------------------- */
+/* K3: upload (nz,ny,nx) x-fastest uint8, build the zero-padded device layout,
+ * the 8^3 brick-max map, and the 256-bin histogram (K1). */
+int vx_volume_create_u8(const uint8_t* host, int64_t nx, int64_t ny, int64_t nz,
+                        vx_volume** out);
+/* K3 with the 16-bit rescale of load_raw (volume.py:148-150):
+ * floor(v*255/65535 + 0.5) == (v + 128) / 257 for every v. */
+int vx_volume_create_u16(const uint16_t* host, int64_t nx, int64_t ny, int64_t nz,
+                         vx_volume** out);
+/* same from a device buffer (e.g. a torch tensor) */
+int vx_volume_create_device_u8(const uint8_t* dev, int64_t nx, int64_t ny, int64_t nz,
+                               vx_volume** out);
+int vx_volume_destroy(vx_volume* vol);
+int vx_volume_dims(const vx_volume* vol, int64_t dims_out[3]);
+int vx_volume_read(const vx_volume* vol, uint8_t* host_out); /* compact copy back */
+int vx_volume_device_bytes(const vx_volume* vol, uint64_t* bytes_out);
+
+/* ---- statistics (histogram.py:59-133, metrics.py:26-33) ------------------ */
+/* K1: counts of the volume's voxels (cached at creation). */
+int vx_histogram(vx_volume* vol, uint64_t counts_out[256]);
+/* K1 over n host bytes (uploaded) */
+int vx_histogram_host(const uint8_t* host, uint64_t n, uint64_t counts_out[256]);
+/* K1 over n device bytes, accumulating into dev_counts[256] (not zeroed),
+ * asynchronously on `stream` (cudaStream_t, 0 = the calling thread's stream). */
+int vx_histogram_device(const uint8_t* dev, uint64_t n, uint64_t* dev_counts, void* stream);
+/* K2: exact Otsu threshold (256-bit cross-multiplied argmin, ties -> smallest
+ * T) of histogram.py:59-101; total must be < 2^47. */
+int vx_otsu(const uint64_t counts[256], int32_t* T_out);
+/* K2 on device counts; writes the threshold to dev_T (int32) */
+int vx_otsu_device(const uint64_t* dev_counts, int32_t* dev_T, void* stream);
+/* K6: image entropy of n grey pixels (metrics.py:26-33); also returns counts */
+int vx_image_entropy(const uint8_t* host_pixels, int64_t n, double* H_out,
+                     uint64_t counts_out[256]);
+/* K6 finalisation from a device histogram (numpy pairwise summation order) */
+int vx_entropy_from_counts_device(const uint64_t* dev_counts, uint64_t n, double* dev_H,
+                                  void* stream);
+
+/* ---- render (render.py:188-560) ------------------------------------------ */
+/* K4: one frame; fused K6 image histogram; host outputs. */
+int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render_params* rp,
+              const vx_filter_config* fc, const vx_partition* part, vx_render_out* out);
+/* K4 into device outputs, asynchronous on `stream`.  Outputs are written, not
+ * accumulated, except image_hist / hit_count / samples which are atomically
+ * accumulated (zero them first). */
+int vx_render_device(vx_volume* vol, const vx_ray_setup* rs, const vx_render_params* rp,
+                     const vx_filter_config* fc, const vx_partition* part,
+                     vx_render_out* dev_out, void* stream);
+/* march_ray (render.py:426-464) for n arbitrary rays: origins/dirs FP64 (n,3),
+ * dirs already normalised, per-ray t spans from vx_ray_spans, max_steps per
+ * ray.  Outputs hit (u8), voxel (i32 x3), t (f32), value (f64). */
+int vx_march_rays(vx_volume* vol, const double* origins, const double* dirs,
+                  const double* t_enter, const double* t_exit, const int32_t* max_steps,
+                  int64_t n, const vx_render_params* rp, const vx_filter_config* fc,
+                  uint8_t* hit_out, int32_t* voxel_out, float* t_out, double* value_out);
+/* primary_ray_dirs (render.py:188-201): (H*W,3) FP64 */
+int vx_ray_dirs(const vx_ray_setup* rs, double* dirs_out);
+/* ray_box_spans (render.py:204-230) for n rays from one origin */
+int vx_ray_spans(const double origin[3], const double* dirs, int64_t n, const int64_t dims[3],
+                 double* t_enter_out, double* t_exit_out);
+/* apply_filter_batch (filters.py:230-266): K5, any integer coords */
+int vx_filter_batch(vx_volume* vol, const int64_t* xs, const int64_t* ys, const int64_t* zs,
+                    int64_t n, const vx_filter_config* fc, double* out);
+/* sobel_normal_batch (render.py:360-377): fallback (n,3) used when |g|<1e-12 */
+int vx_sobel_batch(vx_volume* vol, const int64_t* xs, const int64_t* ys, const int64_t* zs,
+                   int64_t n, const double* fallback, double* normals_out);
+/* shade_phong_batch (render.py:385-403) */
+int vx_phong_batch(const double* normals, const double* view_dirs, int64_t n,
+                   const vx_render_params* rp, uint8_t* out);
+
+/* ---- phantom input generator (volume.py:317-368; inputs only) ------------ */
+/* shape kinds: 0 sphere, 1 shell, 2 box; params per shape:
+ * [kind, cx, cy, cz, intensity, radius, thickness, ex, ey, ez] as doubles.
+ * spot_idx: host array of flat indices (rng.uniform_indices) */
+int vx_volume_create_phantom(int64_t nx, int64_t ny, int64_t nz, const double* shapes,
+                             int64_t n_shapes, double noise_sigma, uint64_t noise_seed,
+                             const int64_t* spot_idx, int64_t n_spots, int32_t spot_intensity,
+                             vx_volume** out);
+/* same, into a compact device buffer of nx*ny*nz bytes (histogram sweeps) */
+int vx_phantom_device(uint8_t* dev_out, int64_t nx, int64_t ny, int64_t nz,
+                      const double* shapes, int64_t n_shapes, double noise_sigma,
+                      uint64_t noise_seed, const int64_t* spot_idx, int64_t n_spots,
+                      int32_t spot_intensity, void* stream);
+
+/* ---- diagnostics ---------------------------------------------------------- */
+/* number of kernels this thread launched since the last reset */
+int vx_launch_counter(uint64_t* n_out, int reset);
+/* exact-skip structure for threshold thr: Chebyshev brick distance map
+ * (dims (nbz+2)*(nby+2)*(nbx+2)) copied to host; for tests */
+int vx_volume_distance_map(vx_volume* vol, int32_t thr, uint8_t* host_out, int64_t dims_out[3]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VOXB200_H */

@@ -1,0 +1,217 @@
+"""ctypes binding of libvoxb200.so (include/voxb200.h).
+
+The product path has no CPU fallback: if the shared library is missing or no
+CUDA device is visible, every compute entry point raises ``NativeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libvoxb200.so"
+
+VX_OK, VX_EINVAL, VX_ENOMEM, VX_ECUDA, VX_ERANGE = 0, 1, 2, 3, 5
+
+# filters.py:43-57 order
+KIND_CODES = {
+    "none": 0,
+    "mean": 1,
+    "sigma": 2,
+    "okada": 3,
+    "entropy": 4,
+    "local-cluster": 5,
+}
+
+
+class NativeError(RuntimeError):
+    """The CUDA library failed (or is unavailable)."""
+
+    def __init__(self, code: int, message: str):
+        super().__init__(message)
+        self.code = code
+
+
+class vx_ray_setup(C.Structure):
+    _fields_ = [
+        ("right", C.c_double * 3),
+        ("up", C.c_double * 3),
+        ("fwd", C.c_double * 3),
+        ("origin", C.c_double * 3),
+        ("tan_f", C.c_double),
+        ("aspect", C.c_double),
+        ("width", C.c_int32),
+        ("height", C.c_int32),
+    ]
+
+
+class vx_render_params(C.Structure):
+    _fields_ = [
+        ("step_size", C.c_double),
+        ("max_steps", C.c_int32),
+        ("chunk", C.c_int32),
+        ("need_clip", C.c_int32),
+        ("skip", C.c_int32),
+        ("ambient", C.c_double),
+        ("diffuse", C.c_double),
+        ("specular", C.c_double),
+        ("shininess", C.c_double),
+        ("light", C.c_double * 3),
+        ("background", C.c_int32),
+        ("_pad", C.c_int32),
+    ]
+
+
+class vx_filter_config(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int32),
+        ("kernel_size", C.c_int32),
+        ("cluster_offset", C.c_int32),
+        ("entropy_pairwise", C.c_int32),
+        ("threshold", C.c_double),
+        ("sigma_band", C.c_double),
+        ("okada_threshold", C.c_double),
+        ("entropy_threshold", C.c_double),
+        ("entropy_lut", C.c_double * 256),
+    ]
+
+
+class vx_partition(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32)]
+
+
+class vx_render_out(C.Structure):
+    _fields_ = [
+        ("pixels", C.c_void_p),
+        ("hit_voxel", C.c_void_p),
+        ("hit_t", C.c_void_p),
+        ("hit_value", C.c_void_p),
+        ("intensity", C.c_void_p),
+        ("image_hist", C.c_void_p),
+        ("hit_count", C.c_void_p),
+        ("samples", C.c_void_p),
+        ("trunc_flag", C.c_void_p),
+    ]
+
+
+P = C.c_void_p
+I32, I64, U64, F64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double
+
+# name -> argtypes (all return int unless listed in _RESTYPES)
+SIGNATURES = {
+    "vx_last_error": [],
+    "vx_version": [],
+    "vx_device_count": [P],
+    "vx_set_device": [C.c_int],
+    "vx_synchronize": [],
+    "vx_volume_create_u8": [P, I64, I64, I64, P],
+    "vx_volume_create_u16": [P, I64, I64, I64, P],
+    "vx_volume_create_device_u8": [P, I64, I64, I64, P],
+    "vx_volume_destroy": [P],
+    "vx_volume_dims": [P, P],
+    "vx_volume_read": [P, P],
+    "vx_volume_device_bytes": [P, P],
+    "vx_histogram": [P, P],
+    "vx_histogram_host": [P, U64, P],
+    "vx_histogram_device": [P, U64, P, P],
+    "vx_otsu": [P, P],
+    "vx_otsu_device": [P, P, P],
+    "vx_image_entropy": [P, I64, P, P],
+    "vx_entropy_from_counts_device": [P, U64, P, P],
+    "vx_render": [P, P, P, P, P, P],
+    "vx_render_device": [P, P, P, P, P, P, P],
+    "vx_march_rays": [P, P, P, P, P, P, I64, P, P, P, P, P, P],
+    "vx_ray_dirs": [P, P],
+    "vx_ray_spans": [P, P, I64, P, P, P],
+    "vx_filter_batch": [P, P, P, P, I64, P, P],
+    "vx_sobel_batch": [P, P, P, P, I64, P, P],
+    "vx_phong_batch": [P, P, I64, P, P],
+    "vx_volume_create_phantom": [I64, I64, I64, P, I64, F64, U64, P, I64, I32, P],
+    "vx_phantom_device": [P, I64, I64, I64, P, I64, F64, U64, P, I64, I32, P],
+    "vx_launch_counter": [P, C.c_int],
+    "vx_volume_distance_map": [P, I32, P, P],
+}
+_RESTYPES = {"vx_last_error": C.c_char_p}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load():
+    """Load (building first if the sources are newer) the CUDA library."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if os.environ.get("VOXB200_NO_BUILD") != "1":
+            try:
+                from . import _build
+
+                if _build.needs_build():
+                    _build.build()
+            except Exception as exc:  # nvcc missing on a prebuilt box is fine
+                if not LIB_PATH.exists():
+                    raise NativeError(VX_ECUDA, f"libvoxb200.so unavailable: {exc}") from exc
+        if not LIB_PATH.exists():
+            raise NativeError(VX_ECUDA, f"libvoxb200.so not found at {LIB_PATH}")
+        lib = C.CDLL(str(LIB_PATH))
+        for name, argtypes in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = argtypes
+            fn.restype = _RESTYPES.get(name, C.c_int)
+        _lib = lib
+        return lib
+
+
+def last_error() -> str:
+    msg = load().vx_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, exc_type=None):
+    """Raise on a non-zero status; EINVAL maps to the caller's error type."""
+    if rc == VX_OK:
+        return
+    msg = last_error()
+    if rc == VX_EINVAL and exc_type is not None:
+        raise exc_type(msg)
+    raise NativeError(rc, msg)
+
+
+def call(name: str, *args, exc_type=None):
+    check(getattr(load(), name)(*args), exc_type)
+
+
+_device_ok = None
+
+
+def require_device():
+    """Fail loudly when no CUDA device is visible (no CPU fallback)."""
+    global _device_ok
+    if _device_ok:
+        return
+    n = C.c_int(0)
+    rc = load().vx_device_count(C.byref(n))
+    if rc != VX_OK or n.value < 1:
+        raise NativeError(VX_ECUDA, "no CUDA device visible: the B200 path has no CPU fallback "
+                          f"({last_error() or 'cudaGetDeviceCount returned 0'})")
+    _device_ok = True
+
+
+def ptr(a: np.ndarray | None):
+    if a is None:
+        return None
+    return C.c_void_p(a.ctypes.data)
+
+
+def launches(reset: bool = False) -> int:
+    n = C.c_uint64(0)
+    call("vx_launch_counter", C.byref(n), 1 if reset else 0)
+    return int(n.value)

@@ -1,0 +1,101 @@
+// Internal declarations shared by the libvoxb200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+#include <string>
+
+#include "../../include/voxb200.h"
+
+// Zero apron around the volume (voxels).  Covers the march's +/-1 voxel
+// truncation slop, Sobel (reach 1) and every filter with reach <= VX_PAD-1;
+// larger reach switches the filter to bounds-checked reads (same border
+// policy as grid.py:34-44: reads outside the grid are 0).
+#define VX_PAD 16
+// Empty-space-skipping brick edge (voxels).
+#define VX_BRICK 8
+#define VX_BRICK_SHIFT 3
+// Chebyshev brick-distance cap of the exact-skip map.
+#define VX_DIST_CAP 24
+#define VX_DIST_CACHE 4
+
+// ---------------------------------------------------------------------------
+// error plumbing
+void vx_set_error(const char* fmt, ...);
+int vx_cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+#define VX_CUDA(call)                                                     \
+  do {                                                                    \
+    cudaError_t _e = (call);                                              \
+    if (_e != cudaSuccess) return vx_cuda_fail(_e, #call, __FILE__, __LINE__); \
+  } while (0)
+#define VX_CHECK_LAUNCH()                                                 \
+  do {                                                                    \
+    cudaError_t _e = cudaGetLastError();                                  \
+    if (_e != cudaSuccess) return vx_cuda_fail(_e, "kernel launch", __FILE__, __LINE__); \
+    vx_count_launch();                                                    \
+  } while (0)
+
+cudaStream_t vx_stream();          // per-thread stream
+void vx_count_launch();
+int vx_sm_count();
+
+// ---------------------------------------------------------------------------
+// device view of a volume replica
+struct VolView {
+  const uint8_t* origin;  // voxel (0,0,0) inside the padded allocation
+  int64_t sy, sz;         // byte strides of rows / planes
+  int nx, ny, nz;
+  const uint8_t* dist;    // Chebyshev brick-distance map at brick (0,0,0)
+  int64_t bsy, bsz;       // strides of the brick maps
+};
+
+struct DistEntry {
+  int thr;
+  uint8_t* map;  // allocation (apron included)
+  uint64_t stamp;
+};
+
+struct vx_volume {
+  int nx, ny, nz;
+  int device;
+  uint8_t* alloc;   // padded allocation
+  uint8_t* origin;  // voxel (0,0,0)
+  int64_t px, py, pz;  // padded dims
+  int64_t sy, sz;
+  uint64_t alloc_bytes;
+  // brick max map with a 1-brick apron: dims (nbx+2, nby+2, nbz+2)
+  uint8_t* bmax;
+  int nbx, nby, nbz;
+  int64_t bsy, bsz;
+  uint64_t map_bytes;
+  DistEntry dist[VX_DIST_CACHE];
+  uint64_t stamp;
+  uint64_t counts[256];
+  std::mutex mu;
+};
+
+VolView vx_view(const vx_volume* v, const uint8_t* dist_map);
+// returns the (cached) distance map of thr, building it if needed
+int vx_get_dist_map(vx_volume* v, int thr, const uint8_t** map_out, cudaStream_t s);
+
+// launchers implemented across translation units
+int vx_launch_hist(const uint8_t* dev, uint64_t n, uint64_t* dev_counts, cudaStream_t s);
+int vx_launch_otsu(const uint64_t* dev_counts, int32_t* dev_T, cudaStream_t s);
+int vx_launch_entropy(const uint64_t* dev_counts, uint64_t n, double* dev_H, cudaStream_t s);
+int vx_launch_brick_max(vx_volume* v, cudaStream_t s);
+int vx_launch_dist_map(const vx_volume* v, int thr, uint8_t* map, cudaStream_t s);
+int vx_launch_u16_to_u8(const uint16_t* src, uint8_t* dst, uint64_t n, cudaStream_t s);
+int vx_launch_phantom(uint8_t* dst, int64_t row_pitch, int64_t plane_pitch, int64_t nx,
+                      int64_t ny, int64_t nz, const double* shapes, int64_t n_shapes,
+                      double noise_sigma, uint64_t noise_seed, const int64_t* spot_idx,
+                      int64_t n_spots, int32_t spot_intensity, cudaStream_t s);
+int vx_volume_alloc(int64_t nx, int64_t ny, int64_t nz, vx_volume** out);
+int vx_volume_finish(vx_volume* v, const uint8_t* compact_dev, cudaStream_t s);
+
+// RAII-free device scratch helpers (stream-ordered allocator)
+template <typename T>
+static inline cudaError_t vx_malloc_async(T** p, size_t bytes, cudaStream_t s) {
+  return cudaMallocAsync(reinterpret_cast<void**>(p), bytes ? bytes : 16, s);
+}

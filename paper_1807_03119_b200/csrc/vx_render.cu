@@ -1,0 +1,1184 @@
+// K4 first-hit ray caster with fused per-hit filter, Sobel normal, Phong
+// shading and image histogram; K5 standalone filter batch; ray setup,
+// march_ray, Sobel and Phong batch entry points.
+//
+// Exact-arithmetic contract (reproduces render.py bit for bit; SURVEY.md
+// Appendix A):
+//   * ray setup in FP64 with numpy's operation order      render.py:188-230
+//   * FP32 march, separate round-to-nearest mul/add (no FMA: this TU is also
+//     built with -fmad=false), truncation toward zero, chunked t
+//     accumulation: t_k = fl(base + fl(s*k)), base += fl(f32(m)*s)
+//                                                            render.py:236-339
+//   * integer filter sums, FP64 quotient                     filters.py:165-227
+//   * exact-integer Sobel gradient, FP64 normal + Phong       render.py:344-403
+//
+// Exact empty-space skipping: a sample can only become a surface candidate
+// when raw >= thr = ceil(T) (render.py:258,307).  The volume carries an 8^3
+// brick-max map; per thr we build the Chebyshev brick distance D to the
+// nearest brick whose max reaches thr.  At the start of a chunk, if the
+// chunk's first sample lies in a brick with D >= 2, every sample whose t is
+// within 8(D-1) - 1/16 voxel of it lies in bricks of max < thr (its
+// truncated voxel is within D-1 bricks; FP32 rounding of the positions is
+// < 2^-7 voxel for volumes up to 8192^3), so those chunks are advanced with
+// the exact FP32 base recurrence and never sampled.  Result-neutral by
+// construction; disabled automatically when thr == 0 (every brick occupied).
+
+#include <climits>
+
+#include "vx_internal.cuh"
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// kernel-argument structs (passed by value)
+
+struct RayCamD {
+  double right[3], up[3], fwd[3], origin[3];
+  double tan_f, aspect;
+  int W, H;
+};
+
+struct MarchD {
+  float s;        // f32(step)
+  float adv;      // fl(f32(chunk) * s)
+  float sk[16];   // fl(s * k), k < chunk
+  float xmax, ymax, zmax;
+  int chunk;
+  int need_clip;
+  int explicit_max;  // > 0: exact frame budget; 0: per-ray guard
+  int thr;           // ceil(T) in [0, 255]
+  int skip;
+  double T;
+  double step;       // FP64 step (per-ray guard)
+};
+
+struct FiltD {
+  int kind;
+  int M;        // kernel size
+  int d;        // cluster offset
+  int pairwise; // entropy sum order (K5, single coordinate)
+  double band, okada_t, entropy_t;
+};
+
+struct ShadeD {
+  double ka, kd, ks, shin;
+  double l[3];
+  int background;
+};
+
+struct OutD {
+  uint8_t* pixels;
+  int32_t* hit_voxel;
+  float* hit_t;
+  double* hit_value;
+  double* intensity;
+  unsigned long long* image_hist;
+  unsigned long long* hit_count;
+  unsigned long long* samples;
+  int32_t* trunc_flag;
+};
+
+struct RenderArgs {
+  VolView V;
+  RayCamD C;
+  MarchD M;
+  FiltD F;
+  ShadeD S;
+  OutD O;
+  int rank, world, tiles_x, n_tiles;
+  double lut[256];
+};
+
+constexpr int kTileW = 8;
+constexpr int kTileH = 16;
+
+// ---------------------------------------------------------------------------
+// voxel access
+
+template <bool CHECKED>
+__device__ __forceinline__ int rd(const VolView& V, long long x, long long y, long long z) {
+  if (CHECKED) {
+    if (x < 0 || y < 0 || z < 0 || x >= V.nx || y >= V.ny || z >= V.nz) return 0;
+  }
+  return __ldg(V.origin + (z * V.sz + y * V.sy + x));
+}
+
+// ---------------------------------------------------------------------------
+// filters (filters.py:165-227); integer sums, FP64 quotient
+
+__device__ double pairwise_sum(const double* a, int n);
+
+template <bool CHECKED>
+__device__ double filter_lc(const VolView& V, const FiltD& F, long long x, long long y,
+                            long long z) {
+  long long sum = 0;
+  const int h = (F.M - 1) >> 1;
+#pragma unroll 1
+  for (int c = 0; c < 9; ++c) {
+    long long cx = x, cy = y, cz = z;
+    if (c > 0) {
+      const int q = c - 1;  // (sx, sy, sz) in {-1,1}^3, filters.py:161
+      cx += ((q >> 2) & 1 ? F.d : -F.d);
+      cy += ((q >> 1) & 1 ? F.d : -F.d);
+      cz += (q & 1 ? F.d : -F.d);
+    }
+    if (h == 1) {
+      // M = 3: arms {c-1, c, c+1} per axis -> centre counted three times
+      sum += 3 * rd<CHECKED>(V, cx, cy, cz) + rd<CHECKED>(V, cx - 1, cy, cz) +
+             rd<CHECKED>(V, cx + 1, cy, cz) + rd<CHECKED>(V, cx, cy - 1, cz) +
+             rd<CHECKED>(V, cx, cy + 1, cz) + rd<CHECKED>(V, cx, cy, cz - 1) +
+             rd<CHECKED>(V, cx, cy, cz + 1);
+    } else {
+      for (int i = -h; i <= h; ++i)
+        sum += rd<CHECKED>(V, cx + i, cy, cz) + rd<CHECKED>(V, cx, cy + i, cz) +
+               rd<CHECKED>(V, cx, cy, cz + i);
+    }
+  }
+  return __ddiv_rn((double)sum, (double)(27 * F.M));
+}
+
+template <bool CHECKED>
+__device__ double filter_mean(const VolView& V, const FiltD& F, long long x, long long y,
+                              long long z) {
+  const int h = (F.M - 1) >> 1;
+  long long sum = 0;
+  for (int dz = -h; dz <= h; ++dz)
+    for (int dy = -h; dy <= h; ++dy)
+      for (int dx = -h; dx <= h; ++dx) sum += rd<CHECKED>(V, x + dx, y + dy, z + dz);
+  return __ddiv_rn((double)sum, (double)(F.M * F.M * F.M));
+}
+
+template <bool CHECKED>
+__device__ double filter_sigma(const VolView& V, const FiltD& F, long long x, long long y,
+                               long long z) {
+  const int h = (F.M - 1) >> 1;
+  const int c = rd<CHECKED>(V, x, y, z);
+  long long sum = 0;
+  long long cnt = 0;
+  for (int dz = -h; dz <= h; ++dz)
+    for (int dy = -h; dy <= h; ++dy)
+      for (int dx = -h; dx <= h; ++dx) {
+        const int v = rd<CHECKED>(V, x + dx, y + dy, z + dz);
+        const int diff = v > c ? v - c : c - v;
+        if ((double)diff <= F.band) {
+          sum += v;
+          ++cnt;
+        }
+      }
+  return __ddiv_rn((double)sum, (double)cnt);  // centre always qualifies
+}
+
+template <bool CHECKED>
+__device__ double filter_okada(const VolView& V, const FiltD& F, long long x, long long y,
+                               long long z) {
+  const int c = rd<CHECKED>(V, x, y, z);
+  const int nb[6] = {rd<CHECKED>(V, x - 1, y, z), rd<CHECKED>(V, x + 1, y, z),
+                     rd<CHECKED>(V, x, y - 1, z), rd<CHECKED>(V, x, y + 1, z),
+                     rd<CHECKED>(V, x, y, z - 1), rd<CHECKED>(V, x, y, z + 1)};
+  long long total = 0;
+  int n = 0;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const int diff = c > nb[k] ? c - nb[k] : nb[k] - c;
+    if ((double)diff < F.okada_t) {
+      total += nb[k];
+      ++n;
+    }
+  }
+  return n > 0 ? __ddiv_rn((double)total, (double)n) : 0.0;
+}
+
+template <bool CHECKED, bool PAIRWISE>
+__device__ double filter_entropy(const VolView& V, const FiltD& F, const double* lut,
+                                 long long x, long long y, long long z) {
+  // kernel_offsets order: dx outer, dy, dz inner (filters.py:132-137)
+  const int h = (F.M - 1) >> 1;
+  double H;
+  if (PAIRWISE) {
+    // a single-coordinate batch: numpy sums the contiguous (M^3, 1) column
+    // with pairwise_sum (SURVEY.md Appendix B exp. 7)
+    double terms[343];  // M <= 7 (checked by the host)
+    int k = 0;
+    for (int dx = -h; dx <= h; ++dx)
+      for (int dy = -h; dy <= h; ++dy)
+        for (int dz = -h; dz <= h; ++dz) terms[k++] = lut[rd<CHECKED>(V, x + dx, y + dy, z + dz)];
+    H = pairwise_sum(terms, k);
+  } else {
+    // >= 2 coordinates: row-by-row (sequential) reduction over axis 0
+    bool first = true;
+    H = 0.0;
+    for (int dx = -h; dx <= h; ++dx)
+      for (int dy = -h; dy <= h; ++dy)
+        for (int dz = -h; dz <= h; ++dz) {
+          const double t = lut[rd<CHECKED>(V, x + dx, y + dy, z + dz)];
+          H = first ? t : __dadd_rn(H, t);
+          first = false;
+        }
+  }
+  return H > F.entropy_t ? (double)rd<CHECKED>(V, x, y, z) : 0.0;
+}
+
+// axis_cluster_average_batch (filters.py:177-178): the centre cluster alone
+template <bool CHECKED>
+__device__ double filter_axis(const VolView& V, const FiltD& F, long long x, long long y,
+                              long long z) {
+  const int h = (F.M - 1) >> 1;
+  long long sum = 0;
+  for (int i = -h; i <= h; ++i)
+    sum += rd<CHECKED>(V, x + i, y, z) + rd<CHECKED>(V, x, y + i, z) + rd<CHECKED>(V, x, y, z + i);
+  return __ddiv_rn((double)sum, (double)(3 * F.M));
+}
+
+constexpr int kAxisCluster = 6;  // K5-only kind
+
+template <int KIND, bool CHECKED, bool PAIRWISE = false>
+__device__ __forceinline__ double filter_value(const VolView& V, const FiltD& F, const double* lut,
+                                               long long x, long long y, long long z) {
+  if (KIND == VX_FILTER_NONE) return (double)rd<CHECKED>(V, x, y, z);
+  if (KIND == VX_FILTER_MEAN) return filter_mean<CHECKED>(V, F, x, y, z);
+  if (KIND == VX_FILTER_SIGMA) return filter_sigma<CHECKED>(V, F, x, y, z);
+  if (KIND == VX_FILTER_OKADA) return filter_okada<CHECKED>(V, F, x, y, z);
+  if (KIND == VX_FILTER_ENTROPY) return filter_entropy<CHECKED, PAIRWISE>(V, F, lut, x, y, z);
+  if (KIND == kAxisCluster) return filter_axis<CHECKED>(V, F, x, y, z);
+  return filter_lc<CHECKED>(V, F, x, y, z);
+}
+
+// numpy pairwise_sum (loops_utils.h) for the single-coordinate entropy batch
+__device__ double pairwise_sum(const double* a, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pairwise_sum(a, n2), pairwise_sum(a + n2, n - n2));
+}
+
+// ---------------------------------------------------------------------------
+// ray setup (render.py:188-230)
+
+__device__ __forceinline__ void ray_dir(const RayCamD& C, int i, int j, double d[3]) {
+  const double u = __dmul_rn(
+      __dmul_rn(__dsub_rn(__ddiv_rn(__dmul_rn(2.0, __dadd_rn((double)i, 0.5)), (double)C.W), 1.0),
+                C.tan_f),
+      C.aspect);
+  const double v =
+      __dmul_rn(__dsub_rn(1.0, __ddiv_rn(__dmul_rn(2.0, __dadd_rn((double)j, 0.5)), (double)C.H)),
+                C.tan_f);
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    d[c] = __dadd_rn(__dadd_rn(C.fwd[c], __dmul_rn(u, C.right[c])), __dmul_rn(v, C.up[c]));
+  const double nrm = __dsqrt_rn(
+      __dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])), __dmul_rn(d[2], d[2])));
+#pragma unroll
+  for (int c = 0; c < 3; ++c) d[c] = __ddiv_rn(d[c], nrm);
+}
+
+// NaN-propagating min / max (np.minimum / np.maximum)
+__device__ __forceinline__ double nmin(double a, double b) {
+  return (a != a || b != b) ? __longlong_as_double(0x7ff8000000000000ll) : (a < b ? a : b);
+}
+__device__ __forceinline__ double nmax(double a, double b) {
+  return (a != a || b != b) ? __longlong_as_double(0x7ff8000000000000ll) : (a > b ? a : b);
+}
+
+__device__ __forceinline__ void ray_span(const double o[3], const double d[3], int nx, int ny,
+                                         int nz, double& t_enter, double& t_exit) {
+  const double hi[3] = {__dsub_rn((double)nx, 0.5), __dsub_rn((double)ny, 0.5),
+                        __dsub_rn((double)nz, 0.5)};
+  double tmin = -__longlong_as_double(0x7ff0000000000000ll);
+  double tmax = __longlong_as_double(0x7ff0000000000000ll);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double near, far;
+    if (d[a] == 0.0) {
+      const bool inside = (-0.5 <= o[a]) && (o[a] <= hi[a]);
+      near = inside ? -__longlong_as_double(0x7ff0000000000000ll)
+                    : __longlong_as_double(0x7ff0000000000000ll);
+      far = -near;
+    } else {
+      const double inv = __ddiv_rn(1.0, d[a]);
+      const double t1 = __dmul_rn(__dsub_rn(-0.5, o[a]), inv);
+      const double t2 = __dmul_rn(__dsub_rn(hi[a], o[a]), inv);
+      near = nmin(t1, t2);
+      far = nmax(t1, t2);
+    }
+    tmin = nmax(tmin, near);
+    tmax = nmin(tmax, far);
+  }
+  t_enter = nmax(tmin, 0.0);
+  t_exit = tmax;
+}
+
+// ---------------------------------------------------------------------------
+// the exact FP32 march (render.py:236-339) with exact skipping
+
+struct RayState {
+  float o[3];  // f32(origin + 0.5)
+  float d[3];  // f32(dir)
+  float base;
+  float tend;
+};
+
+__device__ __forceinline__ float pos1(float o, float t, float d) {
+  return __fadd_rn(o, __fmul_rn(t, d));
+}
+
+__device__ __forceinline__ float clip1(float p, float hi) {
+  // np.clip(p, 0, hi)
+  return p < 0.0f ? 0.0f : (p > hi ? hi : p);
+}
+
+enum MarchStatus { kMiss = 0, kHit = 1, kExhausted = 2 };
+
+// march one ray; limit = sample budget.  Returns kHit on an accepted hit,
+// kMiss when the ray leaves its span, kExhausted when the budget ran out.
+template <int KIND, bool CHECKED>
+__device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const double* lut,
+                      RayState& R, int limit, int& hx, int& hy, int& hz, float& ht,
+                      double& hval, int& hidx, unsigned& nsamp) {
+  int done = 0;
+  float base = R.base;
+  const float tend = R.tend;
+  while (done < limit) {
+    int m = limit - done;
+    if (m > M.chunk) m = M.chunk;
+    if (M.skip && m == M.chunk) {
+      const int vx = __float2int_rz(pos1(R.o[0], base, R.d[0]));
+      const int vy = __float2int_rz(pos1(R.o[1], base, R.d[1]));
+      const int vz = __float2int_rz(pos1(R.o[2], base, R.d[2]));
+      const int bx = vx >> VX_BRICK_SHIFT, by = vy >> VX_BRICK_SHIFT, bz = vz >> VX_BRICK_SHIFT;
+      int D = 0;
+      if (bx >= -1 && by >= -1 && bz >= -1 && bx <= ((V.nx + 7) >> 3) && by <= ((V.ny + 7) >> 3) &&
+          bz <= ((V.nz + 7) >> 3))
+        D = __ldg(V.dist + (bz * V.bsz + by * V.bsy + bx));
+      if (D >= 2) {
+        const float lim = __fadd_rd(base, (float)(VX_BRICK * (D - 1)) - 0.0625f);
+        const float last = M.sk[M.chunk - 1];
+        bool skipped = false;
+        while (__fadd_rn(base, last) <= lim) {
+          base = __fadd_rn(base, M.adv);
+          done += M.chunk;
+          skipped = true;
+          if (!(base <= tend)) return kMiss;
+          if (limit - done < M.chunk) break;  // keep budget tails exact
+        }
+        if (skipped) continue;
+      }
+    }
+    // exact samples of this chunk (render.py:295-329)
+    uint32_t cand = 0;
+#pragma unroll 4
+    for (int k = 0; k < m; ++k) {
+      const float tk = __fadd_rn(base, M.sk[k]);
+      if (!(tk <= tend)) break;  // t_k is monotone in k
+      float px = pos1(R.o[0], tk, R.d[0]);
+      float py = pos1(R.o[1], tk, R.d[1]);
+      float pz = pos1(R.o[2], tk, R.d[2]);
+      if (M.need_clip) {
+        px = clip1(px, M.xmax);
+        py = clip1(py, M.ymax);
+        pz = clip1(pz, M.zmax);
+      }
+      const int raw = rd<false>(V, __float2int_rz(px), __float2int_rz(py), __float2int_rz(pz));
+      ++nsamp;
+      if (raw >= M.thr) cand |= 1u << k;
+    }
+    while (cand) {
+      const int k = __ffs(cand) - 1;
+      cand &= cand - 1;
+      const float tk = __fadd_rn(base, M.sk[k]);
+      float px = pos1(R.o[0], tk, R.d[0]);
+      float py = pos1(R.o[1], tk, R.d[1]);
+      float pz = pos1(R.o[2], tk, R.d[2]);
+      if (M.need_clip) {
+        px = clip1(px, M.xmax);
+        py = clip1(py, M.ymax);
+        pz = clip1(pz, M.zmax);
+      }
+      const int cx = __float2int_rz(px), cy = __float2int_rz(py), cz = __float2int_rz(pz);
+      const double f = filter_value<KIND, CHECKED>(V, F, lut, cx, cy, cz);
+      if (f >= M.T) {
+        hx = cx; hy = cy; hz = cz;
+        ht = tk;
+        hval = f;
+        hidx = done + k;
+        return kHit;
+      }
+    }
+    base = __fadd_rn(base, __fmul_rn((float)m, M.s));
+    done += m;
+    if (!(base <= tend)) return kMiss;
+  }
+  return kExhausted;
+}
+
+// ---------------------------------------------------------------------------
+// Sobel (render.py:344-377) and Phong (render.py:385-403)
+
+template <bool CHECKED>
+__device__ void sobel(const VolView& V, long long x, long long y, long long z, const double fb[3],
+                      double n[3]) {
+  int gx = 0, gy = 0, gz = 0;
+#pragma unroll
+  for (int dx = -1; dx <= 1; ++dx)
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+      for (int dz = -1; dz <= 1; ++dz) {
+        const int v = rd<CHECKED>(V, x + dx, y + dy, z + dz);
+        const int sx = dx == 0 ? 2 : 1, sy = dy == 0 ? 2 : 1, sz = dz == 0 ? 2 : 1;
+        gx += dx * sy * sz * v;
+        gy += dy * sx * sz * v;
+        gz += dz * sx * sy * v;
+      }
+  const double g0 = gx, g1 = gy, g2 = gz;
+  const double nrm =
+      __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(g0, g0), __dmul_rn(g1, g1)), __dmul_rn(g2, g2)));
+  if (nrm < 1e-12) {
+    n[0] = fb[0]; n[1] = fb[1]; n[2] = fb[2];
+  } else {
+    n[0] = __ddiv_rn(-g0, nrm);
+    n[1] = __ddiv_rn(-g1, nrm);
+    n[2] = __ddiv_rn(-g2, nrm);
+  }
+}
+
+// n.l follows the reference host's OpenBLAS dgemv (fma(n2,l2, fma(n0,l0, n1*l1)),
+// measured bit-exact on 20k random vectors); r.v follows numpy einsum
+// ((r0 v0 + r2 v2) + r1 v1).  See DESIGN.md "shading order".
+__device__ __forceinline__ double phong_intensity(const double n[3], const double v[3],
+                                                  const ShadeD& S) {
+  const double ndotl = __fma_rn(n[2], S.l[2], __fma_rn(n[0], S.l[0], __dmul_rn(n[1], S.l[1])));
+  const double k2 = __dmul_rn(2.0, ndotl);
+  const double r0 = __dsub_rn(__dmul_rn(k2, n[0]), S.l[0]);
+  const double r1 = __dsub_rn(__dmul_rn(k2, n[1]), S.l[1]);
+  const double r2 = __dsub_rn(__dmul_rn(k2, n[2]), S.l[2]);
+  const double rdotv = __dadd_rn(__dadd_rn(__dmul_rn(r0, v[0]), __dmul_rn(r2, v[2])), __dmul_rn(r1, v[1]));
+  const double dif = ndotl > 0.0 ? ndotl : 0.0;
+  const double spe = rdotv > 0.0 ? rdotv : 0.0;
+  return __dadd_rn(__dadd_rn(S.ka, __dmul_rn(S.kd, dif)), __dmul_rn(S.ks, pow(spe, S.shin)));
+}
+
+__device__ __forceinline__ uint8_t quantise(double I) {
+  const double c = I < 0.0 ? 0.0 : (I > 1.0 ? 1.0 : I);
+  return (uint8_t)floor(__dadd_rn(__dmul_rn(c, 255.0), 0.5));
+}
+
+// per-ray budget guard: max(1, ceil(span/step) + 1) (render.py:469-473)
+__device__ __forceinline__ int own_budget(double te, double tx, double step) {
+  const double span = __dsub_rn(tx, te);
+  const double q = ceil(__ddiv_rn(span, step));
+  if (!(q <= 2.0e9)) return INT_MAX;
+  int b = (int)q + 1;
+  return b < 1 ? 1 : b;
+}
+
+// ---------------------------------------------------------------------------
+// K4
+
+template <int KIND, bool CHECKED>
+__global__ void __launch_bounds__(kTileW * kTileH) raycast_kernel(const RenderArgs a) {
+  __shared__ double lut[KIND == VX_FILTER_ENTROPY ? 256 : 1];
+  __shared__ unsigned int hist[256];
+  const int tid = threadIdx.y * kTileW + threadIdx.x;
+  if (KIND == VX_FILTER_ENTROPY)
+    for (int i = tid; i < 256; i += kTileW * kTileH) lut[i] = a.lut[i];
+  if (a.O.image_hist)
+    for (int i = tid; i < 256; i += kTileW * kTileH) hist[i] = 0u;
+  __syncthreads();
+
+  const int tile = a.rank + a.world * (int)blockIdx.x;
+  const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+  const int i = tx * kTileW + threadIdx.x;
+  const int j = ty * kTileH + threadIdx.y;
+  const bool valid = tile < a.n_tiles && i < a.C.W && j < a.C.H;
+
+  bool hit = false;
+  unsigned nsamp = 0;
+  if (valid) {
+    double d[3];
+    ray_dir(a.C, i, j, d);
+    double te, tx_;
+    ray_span(a.C.origin, d, a.V.nx, a.V.ny, a.V.nz, te, tx_);
+    int hx = -1, hy = -1, hz = -1, hidx = 0;
+    float ht = 0.0f;
+    double hval = 0.0;
+    if (tx_ >= te && a.M.thr <= 255) {
+      RayState R;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        R.o[c] = __double2float_rn(__dadd_rn(a.C.origin[c], 0.5));
+        R.d[c] = __double2float_rn(d[c]);
+      }
+      R.base = __double2float_rn(te);
+      R.tend = __double2float_rn(tx_);
+      // Per-ray budget = this ray's own max(1, ceil(span/step) + 1) <= the
+      // frame-wide budget of render.py:469-473.  A ray that ends (hit or exit)
+      // within it behaves exactly as under the frame budget; one that exhausts
+      // it is flagged and the host re-renders with the exact frame budget.
+      const int limit = a.M.explicit_max > 0 ? a.M.explicit_max : own_budget(te, tx_, a.M.step);
+      const int st = march<KIND, CHECKED>(a.V, a.M, a.F, lut, R, limit, hx, hy, hz, ht, hval, hidx, nsamp);
+      hit = st == kHit;
+      if (st == kExhausted && a.M.explicit_max <= 0 && a.O.trunc_flag) atomicOr(a.O.trunc_flag, 1);
+    }
+    const size_t p = (size_t)j * a.C.W + i;
+    uint8_t pix = (uint8_t)a.S.background;
+    double I = -1.0;
+    if (hit) {
+      const double view[3] = {-d[0], -d[1], -d[2]};
+      double n[3];
+      sobel<CHECKED>(a.V, hx, hy, hz, view, n);
+      I = phong_intensity(n, view, a.S);
+      pix = quantise(I);
+    }
+    a.O.pixels[p] = pix;
+    if (a.O.hit_voxel) {
+      a.O.hit_voxel[3 * p] = hit ? hx : -1;
+      a.O.hit_voxel[3 * p + 1] = hit ? hy : -1;
+      a.O.hit_voxel[3 * p + 2] = hit ? hz : -1;
+    }
+    if (a.O.hit_t) a.O.hit_t[p] = hit ? ht : 0.0f;
+    if (a.O.hit_value) a.O.hit_value[p] = hit ? hval : 0.0;
+    if (a.O.intensity) a.O.intensity[p] = I;
+    if (a.O.image_hist) atomicAdd(&hist[pix], 1u);
+  }
+  const int nhit = __syncthreads_count(hit);
+  if (tid == 0 && a.O.hit_count && nhit) atomicAdd(a.O.hit_count, (unsigned long long)nhit);
+  if (a.O.samples) {
+    unsigned s = nsamp;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((tid & 31) == 0 && s) atomicAdd(a.O.samples, (unsigned long long)s);
+  }
+  if (a.O.image_hist) {
+    for (int b = tid; b < 256; b += kTileW * kTileH)
+      if (hist[b]) atomicAdd(a.O.image_hist + b, (unsigned long long)hist[b]);
+  }
+}
+
+// frame-wide longest span (render.py:469-473), exact fallback budget
+__global__ void span_max_kernel(const RayCamD C, int nx, int ny, int nz,
+                                unsigned long long* __restrict__ out_bits) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  double span = 0.0;
+  if (p < C.W * C.H) {
+    double d[3];
+    ray_dir(C, p % C.W, p / C.W, d);
+    double te, tx;
+    ray_span(C.origin, d, nx, ny, nz, te, tx);
+    if (tx >= te) span = __dsub_rn(tx, te);
+  }
+  // non-negative doubles order like their bit patterns
+  unsigned long long b = (unsigned long long)__double_as_longlong(span);
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long ob = __shfl_xor_sync(0xffffffffu, b, o);
+    b = ob > b ? ob : b;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(out_bits, b);
+}
+
+// ---------------------------------------------------------------------------
+// march_ray (render.py:426-464) for arbitrary rays
+
+template <int KIND, bool CHECKED>
+__global__ void march_rays_kernel(VolView V, MarchD M, FiltD F, const double* __restrict__ lut_g,
+                                  const double* __restrict__ origins, const double* __restrict__ dirs,
+                                  const double* __restrict__ t_enter, const double* __restrict__ t_exit,
+                                  const int32_t* __restrict__ max_steps, int64_t n,
+                                  uint8_t* hit_out, int32_t* voxel_out, float* t_out,
+                                  double* value_out) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  bool hit = false;
+  int hx = -1, hy = -1, hz = -1, hidx = 0;
+  float ht = 0.0f;
+  double hval = 0.0;
+  unsigned nsamp = 0;
+  const double te = t_enter[r], tx = t_exit[r];
+  if (tx >= te && M.thr <= 255) {
+    RayState R;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      R.o[c] = __double2float_rn(__dadd_rn(origins[3 * r + c], 0.5));
+      R.d[c] = __double2float_rn(dirs[3 * r + c]);
+    }
+    R.base = __double2float_rn(te);
+    R.tend = __double2float_rn(tx);
+    hit = march<KIND, CHECKED>(V, M, F, lut_g, R, max_steps[r], hx, hy, hz, ht, hval, hidx, nsamp) == kHit;
+  }
+  hit_out[r] = hit ? 1 : 0;
+  voxel_out[3 * r] = hx;
+  voxel_out[3 * r + 1] = hy;
+  voxel_out[3 * r + 2] = hz;
+  t_out[r] = ht;
+  value_out[r] = hval;
+}
+
+// K5 apply_filter_batch (filters.py:230-266)
+template <int KIND>
+__global__ void filter_batch_kernel(VolView V, FiltD F, const double* __restrict__ lut,
+                                    const int64_t* __restrict__ xs, const int64_t* __restrict__ ys,
+                                    const int64_t* __restrict__ zs, int64_t n, double* out) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  out[r] = F.pairwise ? filter_value<KIND, true, true>(V, F, lut, xs[r], ys[r], zs[r])
+                     : filter_value<KIND, true, false>(V, F, lut, xs[r], ys[r], zs[r]);
+}
+
+__global__ void sobel_batch_kernel(VolView V, const int64_t* __restrict__ xs,
+                                   const int64_t* __restrict__ ys, const int64_t* __restrict__ zs,
+                                   int64_t n, const double* __restrict__ fb, double* out) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const double f[3] = {fb[3 * r], fb[3 * r + 1], fb[3 * r + 2]};
+  double nn[3];
+  sobel<true>(V, xs[r], ys[r], zs[r], f, nn);
+  out[3 * r] = nn[0];
+  out[3 * r + 1] = nn[1];
+  out[3 * r + 2] = nn[2];
+}
+
+__global__ void phong_batch_kernel(const double* __restrict__ normals, const double* __restrict__ views,
+                                   int64_t n, ShadeD S, uint8_t* out) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const double nn[3] = {normals[3 * r], normals[3 * r + 1], normals[3 * r + 2]};
+  const double v[3] = {views[3 * r], views[3 * r + 1], views[3 * r + 2]};
+  out[r] = quantise(phong_intensity(nn, v, S));
+}
+
+__global__ void ray_dirs_kernel(RayCamD C, double* out) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= (int64_t)C.W * C.H) return;
+  double d[3];
+  ray_dir(C, (int)(p % C.W), (int)(p / C.W), d);
+  out[3 * p] = d[0];
+  out[3 * p + 1] = d[1];
+  out[3 * p + 2] = d[2];
+}
+
+__global__ void ray_spans_kernel(double o0, double o1, double o2, const double* __restrict__ dirs,
+                                 int64_t n, int nx, int ny, int nz, double* te, double* tx) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const double o[3] = {o0, o1, o2};
+  const double d[3] = {dirs[3 * r], dirs[3 * r + 1], dirs[3 * r + 2]};
+  ray_span(o, d, nx, ny, nz, te[r], tx[r]);
+}
+
+// ---------------------------------------------------------------------------
+// host-side helpers
+
+RayCamD make_cam(const vx_ray_setup* rs) {
+  RayCamD C;
+  for (int c = 0; c < 3; ++c) {
+    C.right[c] = rs->right[c];
+    C.up[c] = rs->up[c];
+    C.fwd[c] = rs->fwd[c];
+    C.origin[c] = rs->origin[c];
+  }
+  C.tan_f = rs->tan_f;
+  C.aspect = rs->aspect;
+  C.W = rs->width;
+  C.H = rs->height;
+  return C;
+}
+
+int make_march(const vx_volume* v, const vx_render_params* rp, const vx_filter_config* fc,
+               MarchD& M) {
+  if (!(rp->step_size > 0.0)) {
+    vx_set_error("step_size must be > 0, got %g", rp->step_size);
+    return VX_EINVAL;
+  }
+  if (rp->chunk < 1 || rp->chunk > 16) {
+    vx_set_error("chunk must be in [1, 16], got %d", rp->chunk);
+    return VX_EINVAL;
+  }
+  M.s = (float)rp->step_size;  // np.float32(step): round to nearest
+  for (int k = 0; k < 16; ++k) M.sk[k] = M.s * (float)k;
+  M.adv = (float)rp->chunk * M.s;
+  M.xmax = (float)v->nx;
+  M.ymax = (float)v->ny;
+  M.zmax = (float)v->nz;
+  M.chunk = rp->chunk;
+  M.need_clip = rp->need_clip;
+  M.explicit_max = rp->max_steps > 0 ? rp->max_steps : 0;
+  double T = fc->threshold;
+  double c = ceil(T);
+  int thr = c < 0.0 ? 0 : (c > 256.0 ? 256 : (int)c);  // max(0, ceil(T)); >255 = no hits
+  M.thr = thr;
+  M.T = T;
+  M.step = rp->step_size;
+  M.skip = rp->skip && thr > 0 && thr <= 255;
+  return VX_OK;
+}
+
+int make_filter(const vx_filter_config* fc, FiltD& F, bool batch_api = false) {
+  if (fc->kind < 0 || fc->kind > (batch_api ? kAxisCluster : 5)) {
+    vx_set_error("unhandled filter kind %d", fc->kind);
+    return VX_EINVAL;
+  }
+  if (fc->kernel_size < 3 || (fc->kernel_size & 1) == 0) {
+    vx_set_error("kernel_size must be odd and >= 3, got %d", fc->kernel_size);
+    return VX_EINVAL;
+  }
+  if (fc->cluster_offset < 1) {
+    vx_set_error("cluster_offset must be >= 1, got %d", fc->cluster_offset);
+    return VX_EINVAL;
+  }
+  F.kind = fc->kind;
+  F.M = fc->kernel_size;
+  F.d = fc->cluster_offset;
+  F.pairwise = fc->entropy_pairwise;
+  F.band = fc->sigma_band;
+  F.okada_t = fc->okada_threshold;
+  F.entropy_t = fc->entropy_threshold;
+  if (F.pairwise && F.M > 7) {
+    vx_set_error("pairwise entropy order supports kernel_size <= 7");
+    return VX_EINVAL;
+  }
+  return VX_OK;
+}
+
+int filter_reach(const FiltD& F) {
+  const int h = (F.M - 1) / 2;
+  if (F.kind == VX_FILTER_LOCAL_CLUSTER) return h + F.d;
+  if (F.kind == VX_FILTER_OKADA) return 1;
+  if (F.kind == VX_FILTER_NONE) return 0;
+  return h;
+}
+
+ShadeD make_shade(const vx_render_params* rp) {
+  ShadeD S;
+  S.ka = rp->ambient;
+  S.kd = rp->diffuse;
+  S.ks = rp->specular;
+  S.shin = rp->shininess;
+  for (int c = 0; c < 3; ++c) S.l[c] = rp->light[c];
+  S.background = rp->background;
+  return S;
+}
+
+template <int KIND, bool CHECKED>
+void launch_raycast(const RenderArgs& a, int grid, cudaStream_t s) {
+  raycast_kernel<KIND, CHECKED><<<grid, dim3(kTileW, kTileH), 0, s>>>(a);
+}
+
+template <bool CHECKED>
+void dispatch_raycast(const RenderArgs& a, int grid, cudaStream_t s) {
+  switch (a.F.kind) {
+    case VX_FILTER_NONE: launch_raycast<VX_FILTER_NONE, CHECKED>(a, grid, s); break;
+    case VX_FILTER_MEAN: launch_raycast<VX_FILTER_MEAN, CHECKED>(a, grid, s); break;
+    case VX_FILTER_SIGMA: launch_raycast<VX_FILTER_SIGMA, CHECKED>(a, grid, s); break;
+    case VX_FILTER_OKADA: launch_raycast<VX_FILTER_OKADA, CHECKED>(a, grid, s); break;
+    case VX_FILTER_ENTROPY: launch_raycast<VX_FILTER_ENTROPY, CHECKED>(a, grid, s); break;
+    default: launch_raycast<VX_FILTER_LOCAL_CLUSTER, CHECKED>(a, grid, s); break;
+  }
+}
+
+template <bool CHECKED>
+void dispatch_march(const VolView& V, const MarchD& M, const FiltD& F, const double* lut,
+                    const double* o, const double* d, const double* te, const double* tx,
+                    const int32_t* ms, int64_t n, uint8_t* h, int32_t* vox, float* t, double* val,
+                    cudaStream_t s) {
+  const int bs = 128;
+  const unsigned g = (unsigned)((n + bs - 1) / bs);
+#define VX_MR(K) march_rays_kernel<K, CHECKED><<<g, bs, 0, s>>>(V, M, F, lut, o, d, te, tx, ms, n, h, vox, t, val)
+  switch (F.kind) {
+    case VX_FILTER_NONE: VX_MR(VX_FILTER_NONE); break;
+    case VX_FILTER_MEAN: VX_MR(VX_FILTER_MEAN); break;
+    case VX_FILTER_SIGMA: VX_MR(VX_FILTER_SIGMA); break;
+    case VX_FILTER_OKADA: VX_MR(VX_FILTER_OKADA); break;
+    case VX_FILTER_ENTROPY: VX_MR(VX_FILTER_ENTROPY); break;
+    default: VX_MR(VX_FILTER_LOCAL_CLUSTER); break;
+  }
+#undef VX_MR
+}
+
+// scratch buffer freed on scope exit (stream ordered)
+struct Scratch {
+  void* p = nullptr;
+  cudaStream_t s;
+  explicit Scratch(cudaStream_t st) : s(st) {}
+  ~Scratch() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  template <typename T>
+  T* get() { return reinterpret_cast<T*>(p); }
+};
+
+}  // namespace
+
+// ===========================================================================
+// exported entry points
+
+static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_params* rp,
+                       const vx_filter_config* fc, const vx_partition* part, vx_render_out* o,
+                       cudaStream_t s, int explicit_budget_override) {
+  if (!vol || !rs || !rp || !fc || !o || !o->pixels) {
+    vx_set_error("vx_render: null argument");
+    return VX_EINVAL;
+  }
+  if (rs->width < 1 || rs->height < 1) {
+    vx_set_error("image size must be >= 1x1, got %dx%d", rs->width, rs->height);
+    return VX_EINVAL;
+  }
+  RenderArgs a;
+  a.C = make_cam(rs);
+  int rc = make_march(vol, rp, fc, a.M);
+  if (rc) return rc;
+  if (explicit_budget_override > 0) a.M.explicit_max = explicit_budget_override;
+  rc = make_filter(fc, a.F);
+  if (rc) return rc;
+  a.S = make_shade(rp);
+  for (int i = 0; i < 256; ++i) a.lut[i] = fc->entropy_lut[i];
+  const uint8_t* dist = nullptr;
+  if (a.M.skip) {
+    rc = vx_get_dist_map(vol, a.M.thr, &dist, s);
+    if (rc) return rc;
+  }
+  a.V = vx_view(vol, dist);
+  a.O.pixels = o->pixels;
+  a.O.hit_voxel = o->hit_voxel;
+  a.O.hit_t = o->hit_t;
+  a.O.hit_value = o->hit_value;
+  a.O.intensity = o->intensity;
+  a.O.image_hist = reinterpret_cast<unsigned long long*>(o->image_hist);
+  a.O.hit_count = reinterpret_cast<unsigned long long*>(o->hit_count);
+  a.O.samples = reinterpret_cast<unsigned long long*>(o->samples);
+  a.O.trunc_flag = o->trunc_flag;
+  a.world = part ? part->world : 1;
+  a.rank = part ? part->rank : 0;
+  if (a.world < 1 || a.rank < 0 || a.rank >= a.world) {
+    vx_set_error("bad partition rank %d of %d", a.rank, a.world);
+    return VX_EINVAL;
+  }
+  a.tiles_x = (rs->width + kTileW - 1) / kTileW;
+  const int tiles_y = (rs->height + kTileH - 1) / kTileH;
+  a.n_tiles = a.tiles_x * tiles_y;
+  const int grid = (a.n_tiles - a.rank + a.world - 1) / a.world;
+  if (grid <= 0) return VX_OK;
+  const bool checked = filter_reach(a.F) > VX_PAD - 1;
+  if (checked)
+    dispatch_raycast<true>(a, grid, s);
+  else
+    dispatch_raycast<false>(a, grid, s);
+  VX_CHECK_LAUNCH();
+  return VX_OK;
+}
+
+// exact frame budget of render.py:469-473
+static int frame_budget(vx_volume* vol, const vx_ray_setup* rs, double step, cudaStream_t s,
+                        int* budget) {
+  RayCamD C = make_cam(rs);
+  Scratch sc(s);
+  VX_CUDA(vx_malloc_async(reinterpret_cast<unsigned long long**>(&sc.p), 8, s));
+  VX_CUDA(cudaMemsetAsync(sc.p, 0, 8, s));
+  const int n = rs->width * rs->height;
+  span_max_kernel<<<(n + 255) / 256, 256, 0, s>>>(C, vol->nx, vol->ny, vol->nz,
+                                                   sc.get<unsigned long long>());
+  VX_CHECK_LAUNCH();
+  unsigned long long bits = 0;
+  VX_CUDA(cudaMemcpyAsync(&bits, sc.p, 8, cudaMemcpyDeviceToHost, s));
+  VX_CUDA(cudaStreamSynchronize(s));
+  double longest;
+  memcpy(&longest, &bits, 8);
+  double q = ceil(longest / step);
+  long long b = (long long)q + 1;
+  if (b < 1) b = 1;
+  if (b > INT_MAX) b = INT_MAX;
+  *budget = (int)b;
+  return VX_OK;
+}
+
+extern "C" int vx_render_device(vx_volume* vol, const vx_ray_setup* rs, const vx_render_params* rp,
+                                const vx_filter_config* fc, const vx_partition* part,
+                                vx_render_out* dev_out, void* stream) {
+  cudaStream_t s = stream ? (cudaStream_t)stream : vx_stream();
+  return render_impl(vol, rs, rp, fc, part, dev_out, s, 0);
+}
+
+extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render_params* rp,
+                         const vx_filter_config* fc, const vx_partition* part, vx_render_out* out) {
+  if (!vol || !rs || !rp || !fc || !out || !out->pixels) {
+    vx_set_error("vx_render: null argument");
+    return VX_EINVAL;
+  }
+  if (rs->width < 1 || rs->height < 1) {
+    vx_set_error("image size must be >= 1x1, got %dx%d", rs->width, rs->height);
+    return VX_EINVAL;
+  }
+  cudaStream_t s = vx_stream();
+  const size_t npx = (size_t)rs->width * rs->height;
+  // device staging: pixels | hit_voxel | hit_t | hit_value | intensity | hist | counters
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  const size_t o_pix = take(npx);
+  const size_t o_vox = out->hit_voxel ? take(npx * 12) : 0;
+  const size_t o_t = out->hit_t ? take(npx * 4) : 0;
+  const size_t o_val = out->hit_value ? take(npx * 8) : 0;
+  const size_t o_int = out->intensity ? take(npx * 8) : 0;
+  const size_t o_small = take(256 * 8 + 3 * 8 + 8);
+  Scratch sc(s);
+  VX_CUDA(vx_malloc_async(reinterpret_cast<uint8_t**>(&sc.p), off, s));
+  uint8_t* base = sc.get<uint8_t>();
+  VX_CUDA(cudaMemsetAsync(base + o_small, 0, 256 * 8 + 3 * 8 + 8, s));
+  if (part && part->world > 1) VX_CUDA(cudaMemsetAsync(base + o_pix, 0, npx, s));
+  vx_render_out d;
+  d.pixels = base + o_pix;
+  d.hit_voxel = out->hit_voxel ? reinterpret_cast<int32_t*>(base + o_vox) : nullptr;
+  d.hit_t = out->hit_t ? reinterpret_cast<float*>(base + o_t) : nullptr;
+  d.hit_value = out->hit_value ? reinterpret_cast<double*>(base + o_val) : nullptr;
+  d.intensity = out->intensity ? reinterpret_cast<double*>(base + o_int) : nullptr;
+  uint64_t* small = reinterpret_cast<uint64_t*>(base + o_small);
+  d.image_hist = small;
+  d.hit_count = small + 256;
+  d.samples = small + 257;
+  d.trunc_flag = reinterpret_cast<int32_t*>(small + 258);
+  int rc = render_impl(vol, rs, rp, fc, part, &d, s, 0);
+  if (rc) return rc;
+  uint64_t small_h[259];
+  VX_CUDA(cudaMemcpyAsync(small_h, small, sizeof(small_h), cudaMemcpyDeviceToHost, s));
+  VX_CUDA(cudaStreamSynchronize(s));
+  int32_t flag;
+  memcpy(&flag, &small_h[258], 4);
+  if (flag && rp->max_steps <= 0) {
+    // a ray hit beyond its own span budget: re-render with the exact frame budget
+    int budget = 0;
+    rc = frame_budget(vol, rs, rp->step_size, s, &budget);
+    if (rc) return rc;
+    VX_CUDA(cudaMemsetAsync(small, 0, 259 * 8, s));
+    rc = render_impl(vol, rs, rp, fc, part, &d, s, budget);
+    if (rc) return rc;
+    VX_CUDA(cudaMemcpyAsync(small_h, small, sizeof(small_h), cudaMemcpyDeviceToHost, s));
+  }
+  VX_CUDA(cudaMemcpyAsync(out->pixels, d.pixels, npx, cudaMemcpyDeviceToHost, s));
+  if (out->hit_voxel)
+    VX_CUDA(cudaMemcpyAsync(out->hit_voxel, d.hit_voxel, npx * 12, cudaMemcpyDeviceToHost, s));
+  if (out->hit_t) VX_CUDA(cudaMemcpyAsync(out->hit_t, d.hit_t, npx * 4, cudaMemcpyDeviceToHost, s));
+  if (out->hit_value)
+    VX_CUDA(cudaMemcpyAsync(out->hit_value, d.hit_value, npx * 8, cudaMemcpyDeviceToHost, s));
+  if (out->intensity)
+    VX_CUDA(cudaMemcpyAsync(out->intensity, d.intensity, npx * 8, cudaMemcpyDeviceToHost, s));
+  VX_CUDA(cudaStreamSynchronize(s));
+  if (out->image_hist) memcpy(out->image_hist, small_h, 256 * 8);
+  if (out->hit_count) out->hit_count[0] = small_h[256];
+  if (out->samples) out->samples[0] = small_h[257];
+  if (out->trunc_flag) out->trunc_flag[0] = 0;
+  return VX_OK;
+}
+
+extern "C" int vx_march_rays(vx_volume* vol, const double* origins, const double* dirs,
+                             const double* t_enter, const double* t_exit, const int32_t* max_steps,
+                             int64_t n, const vx_render_params* rp, const vx_filter_config* fc,
+                             uint8_t* hit_out, int32_t* voxel_out, float* t_out,
+                             double* value_out) {
+  if (!vol || !rp || !fc || n < 0) {
+    vx_set_error("vx_march_rays: bad argument");
+    return VX_EINVAL;
+  }
+  if (n == 0) return VX_OK;
+  cudaStream_t s = vx_stream();
+  MarchD M;
+  FiltD F;
+  int rc = make_march(vol, rp, fc, M);
+  if (rc) return rc;
+  rc = make_filter(fc, F);
+  if (rc) return rc;
+  const uint8_t* dist = nullptr;
+  if (M.skip) {
+    rc = vx_get_dist_map(vol, M.thr, &dist, s);
+    if (rc) return rc;
+  }
+  VolView V = vx_view(vol, dist);
+  // one device block: in (o,d,te,tx,ms,lut) out (hit,vox,t,val)
+  const size_t b_o = n * 24, b_te = n * 8, b_ms = n * 4, b_lut = 256 * 8;
+  const size_t b_h = n, b_v = n * 12, b_t = n * 4, b_val = n * 8;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  const size_t oo = take(b_o), od = take(b_o), ote = take(b_te), otx = take(b_te), oms = take(b_ms),
+               olut = take(b_lut), oh = take(b_h), ov = take(b_v), ot = take(b_t), oval = take(b_val);
+  Scratch sc(s);
+  VX_CUDA(vx_malloc_async(reinterpret_cast<uint8_t**>(&sc.p), off, s));
+  uint8_t* b = sc.get<uint8_t>();
+  VX_CUDA(cudaMemcpyAsync(b + oo, origins, b_o, cudaMemcpyHostToDevice, s));
+  VX_CUDA(cudaMemcpyAsync(b + od, dirs, b_o, cudaMemcpyHostToDevice, s));
+  VX_CUDA(cudaMemcpyAsync(b + ote, t_enter, b_te, cudaMemcpyHostToDevice, s));
+  VX_CUDA(cudaMemcpyAsync(b + otx, t_exit, b_te, cudaMemcpyHostToDevice, s));
+  VX_CUDA(cudaMemcpyAsync(b + oms, max_steps, b_ms, cudaMemcpyHostToDevice, s));
+  VX_CUDA(cudaMemcpyAsync(b + olut, fc->entropy_lut, b_lut, cudaMemcpyHostToDevice, s));
+  const bool checked = filter_reach(F) > VX_PAD - 1;
+  auto* pd = reinterpret_cast<const double*>(b + od);
+  auto* po = reinterpret_cast<const double*>(b + oo);
+  if (checked)
+    dispatch_march<true>(V, M, F, reinterpret_cast<const double*>(b + olut), po, pd,
+                         reinterpret_cast<const double*>(b + ote), reinterpret_cast<const double*>(b + otx),
+                         reinterpret_cast<const int32_t*>(b + oms), n, b + oh,
+                         reinterpret_cast<int32_t*>(b + ov), reinterpret_cast<float*>(b + ot),
+                         reinterpret_cast<double*>(b + oval), s);
+  else
+    dispatch_march<false>(V, M, F, reinterpret_cast<const double*>(b + olut), po, pd,
+                          reinterpret_cast<const double*>(b + ote), reinterpret_cast<const double*>(b + otx),
+                          reinterpret_cast<const int32_t*>(b + oms), n, b + oh,
+                          reinterpret_cast<int32_t*>(b + ov), reinterpret_cast<float*>(b + ot),
+                          reinterpret_cast<double*>(b + oval), s);
+  VX_CHECK_LAUNCH();
+  VX_CUDA(cudaMemcpyAsync(hit_out, b + oh, b_h, cudaMemcpyDeviceToHost, s));
+  VX_CUDA(cudaMemcpyAsync(voxel_out, b + ov, b_v, cudaMemcpyDeviceToHost, s));
+  VX_CUDA(cudaMemcpyAsync(t_out, b + ot, b_t, cudaMemcpyDeviceToHost, s));
+  VX_CUDA(cudaMemcpyAsync(value_out, b + oval, b_val, cudaMemcpyDeviceToHost, s));
+  VX_CUDA(cudaStreamSynchronize(s));
+  return VX_OK;
+}
+
+extern "C" int vx_ray_dirs(const vx_ray_setup* rs, double* dirs_out) {
+  if (!rs || !dirs_out || rs->width < 1 || rs->height < 1) {
+    vx_set_error("vx_ray_dirs: bad argument");
+    return VX_EINVAL;
+  }
+  cudaStream_t s = vx_stream();
+  const int64_t n = (int64_t)rs->width * rs->height;
+  Scratch sc(s);
+  VX_CUDA(vx_malloc_async(reinterpret_cast<double**>(&sc.p), n * 24, s));
+  ray_dirs_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(make_cam(rs), sc.get<double>());
+  VX_CHECK_LAUNCH();
+  VX_CUDA(cudaMemcpyAsync(dirs_out, sc.p, n * 24, cudaMemcpyDeviceToHost, s));
+  VX_CUDA(cudaStreamSynchronize(s));
+  return VX_OK;
+}
+
+extern "C" int vx_ray_spans(const double origin[3], const double* dirs, int64_t n,
+                            const int64_t dims[3], double* t_enter_out, double* t_exit_out) {
+  if (!origin || !dirs || !dims || n < 0) {
+    vx_set_error("vx_ray_spans: bad argument");
+    return VX_EINVAL;
+  }
+  if (n == 0) return VX_OK;
+  cudaStream_t s = vx_stream();
+  Scratch sc(s);
+  VX_CUDA(vx_malloc_async(reinterpret_cast<double**>(&sc.p), n * 40, s));
+  double* dd = sc.get<double>();
+  double* te = dd + 3 * n;
+  double* tx = te + n;
+  VX_CUDA(cudaMemcpyAsync(dd, dirs, n * 24, cudaMemcpyHostToDevice, s));
+  ray_spans_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+      origin[0], origin[1], origin[2], dd, n, (int)dims[0], (int)dims[1], (int)dims[2], te, tx);
+  VX_CHECK_LAUNCH();
+  VX_CUDA(cudaMemcpyAsync(t_enter_out, te, n * 8, cudaMemcpyDeviceToHost, s));
+  VX_CUDA(cudaMemcpyAsync(t_exit_out, tx, n * 8, cudaMemcpyDeviceToHost, s));
+  VX_CUDA(cudaStreamSynchronize(s));
+  return VX_OK;
+}
+
+extern "C" int vx_filter_batch(vx_volume* vol, const int64_t* xs, const int64_t* ys,
+                               const int64_t* zs, int64_t n, const vx_filter_config* fc,
+                               double* out) {
+  if (!vol || !fc || n < 0) {
+    vx_set_error("vx_filter_batch: bad argument");
+    return VX_EINVAL;
+  }
+  if (n == 0) return VX_OK;
+  FiltD F;
+  int rc = make_filter(fc, F, true);
+  if (rc) return rc;
+  cudaStream_t s = vx_stream();
+  Scratch sc(s);
+  const size_t bytes = n * 8 * 4 + 256 * 8;
+  VX_CUDA(vx_malloc_async(reinterpret_cast<uint8_t**>(&sc.p), bytes, s));
+  int64_t* dx = sc.get<int64_t>();
+  int64_t* dy = dx + n;
+  int64_t* dz = dy + n;
+  double* dout = reinterpret_cast<double*>(dz + n);
+  double* dlut = dout + n;
+  VX_CUDA(cudaMemcpyAsync(dx, xs, n * 8, cudaMemcpyHostToDevice, s));
+  VX_CUDA(cudaMemcpyAsync(dy, ys, n * 8, cudaMemcpyHostToDevice, s));
+  VX_CUDA(cudaMemcpyAsync(dz, zs, n * 8, cudaMemcpyHostToDevice, s));
+  VX_CUDA(cudaMemcpyAsync(dlut, fc->entropy_lut, 256 * 8, cudaMemcpyHostToDevice, s));
+  VolView V = vx_view(vol, nullptr);
+  const unsigned g = (unsigned)((n + 127) / 128);
+#define VX_FB(K) filter_batch_kernel<K><<<g, 128, 0, s>>>(V, F, dlut, dx, dy, dz, n, dout)
+  switch (F.kind) {
+    case VX_FILTER_NONE: VX_FB(VX_FILTER_NONE); break;
+    case VX_FILTER_MEAN: VX_FB(VX_FILTER_MEAN); break;
+    case VX_FILTER_SIGMA: VX_FB(VX_FILTER_SIGMA); break;
+    case VX_FILTER_OKADA: VX_FB(VX_FILTER_OKADA); break;
+    case VX_FILTER_ENTROPY: VX_FB(VX_FILTER_ENTROPY); break;
+    case kAxisCluster: VX_FB(kAxisCluster); break;
+    default: VX_FB(VX_FILTER_LOCAL_CLUSTER); break;
+  }
+#undef VX_FB
+  VX_CHECK_LAUNCH();
+  VX_CUDA(cudaMemcpyAsync(out, dout, n * 8, cudaMemcpyDeviceToHost, s));
+  VX_CUDA(cudaStreamSynchronize(s));
+  return VX_OK;
+}
+
+extern "C" int vx_sobel_batch(vx_volume* vol, const int64_t* xs, const int64_t* ys,
+                              const int64_t* zs, int64_t n, const double* fallback,
+                              double* normals_out) {
+  if (!vol || n < 0) {
+    vx_set_error("vx_sobel_batch: bad argument");
+    return VX_EINVAL;
+  }
+  if (n == 0) return VX_OK;
+  cudaStream_t s = vx_stream();
+  Scratch sc(s);
+  VX_CUDA(vx_malloc_async(reinterpret_cast<uint8_t**>(&sc.p), n * 8 * 9, s));
+  int64_t* dx = sc.get<int64_t>();
+  int64_t* dy = dx + n;
+  int64_t* dz = dy + n;
+  double* dfb = reinterpret_cast<double*>(dz + n);
+  double* dout = dfb + 3 * n;
+  VX_CUDA(cudaMemcpyAsync(dx, xs, n * 8, cudaMemcpyHostToDevice, s));
+  VX_CUDA(cudaMemcpyAsync(dy, ys, n * 8, cudaMemcpyHostToDevice, s));
+  VX_CUDA(cudaMemcpyAsync(dz, zs, n * 8, cudaMemcpyHostToDevice, s));
+  VX_CUDA(cudaMemcpyAsync(dfb, fallback, n * 24, cudaMemcpyHostToDevice, s));
+  sobel_batch_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(vx_view(vol, nullptr), dx, dy,
+                                                                  dz, n, dfb, dout);
+  VX_CHECK_LAUNCH();
+  VX_CUDA(cudaMemcpyAsync(normals_out, dout, n * 24, cudaMemcpyDeviceToHost, s));
+  VX_CUDA(cudaStreamSynchronize(s));
+  return VX_OK;
+}
+
+extern "C" int vx_phong_batch(const double* normals, const double* view_dirs, int64_t n,
+                              const vx_render_params* rp, uint8_t* out) {
+  if (!rp || n < 0) {
+    vx_set_error("vx_phong_batch: bad argument");
+    return VX_EINVAL;
+  }
+  if (n == 0) return VX_OK;
+  cudaStream_t s = vx_stream();
+  Scratch sc(s);
+  VX_CUDA(vx_malloc_async(reinterpret_cast<uint8_t**>(&sc.p), n * 49, s));
+  double* dn = sc.get<double>();
+  double* dv = dn + 3 * n;
+  uint8_t* dout = reinterpret_cast<uint8_t*>(dv + 3 * n);
+  VX_CUDA(cudaMemcpyAsync(dn, normals, n * 24, cudaMemcpyHostToDevice, s));
+  VX_CUDA(cudaMemcpyAsync(dv, view_dirs, n * 24, cudaMemcpyHostToDevice, s));
+  phong_batch_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(dn, dv, n, make_shade(rp), dout);
+  VX_CHECK_LAUNCH();
+  VX_CUDA(cudaMemcpyAsync(out, dout, n, cudaMemcpyDeviceToHost, s));
+  VX_CUDA(cudaStreamSynchronize(s));
+  return VX_OK;
+}

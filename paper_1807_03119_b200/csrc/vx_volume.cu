@@ -1,0 +1,237 @@
+// K3 volume layout (zero-padded replica + 8^3 brick-max map), the per-thr
+// Chebyshev brick-distance map of the exact skip, the 16-bit rescale of
+// load_raw, and the K7 phantom input generator.
+//
+// Reference: volume.py:122-151 (load_raw), grid.py:22-31 (padded_flat),
+// volume.py:317-368 + rng.py:24-51 (generate_phantom; inputs only).
+
+#include <cstring>
+
+#include "vx_internal.cuh"
+
+namespace {
+
+// one thread per 8^3 brick; rows of 8 voxels are 8-byte aligned (origin and
+// strides are multiples of 16)
+__global__ void brick_max_kernel(const uint8_t* __restrict__ origin, int64_t sy, int64_t sz,
+                                 int nbx, int nby, int nbz, uint8_t* __restrict__ bmax_origin,
+                                 int64_t bsy, int64_t bsz) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nb = (int64_t)nbx * nby * nbz;
+  if (b >= nb) return;
+  const int bx = (int)(b % nbx);
+  const int by = (int)((b / nbx) % nby);
+  const int bz = (int)(b / ((int64_t)nbx * nby));
+  uint32_t m = 0;
+  const uint8_t* p0 = origin + (int64_t)bz * 8 * sz + (int64_t)by * 8 * sy + (int64_t)bx * 8;
+#pragma unroll 2
+  for (int z = 0; z < 8; ++z) {
+#pragma unroll
+    for (int y = 0; y < 8; ++y) {
+      const uint2 w = __ldg(reinterpret_cast<const uint2*>(p0 + z * sz + y * sy));
+      m = max(m, __vmaxu4(w.x, w.y));
+    }
+  }
+  m = max(max(m & 0xffu, (m >> 8) & 0xffu), max((m >> 16) & 0xffu, m >> 24));
+  bmax_origin[(int64_t)bz * bsz + (int64_t)by * bsy + bx] = (uint8_t)m;
+}
+
+// Chebyshev distance transform on the brick grid, separable min-max passes:
+// D(b) = min_o max_i |b_i - o_i| over occupied o = min_oz max(|dz|, min_oy
+// max(|dy|, min_ox |dx|)).  Out-of-map cells are unoccupied; capped.
+__global__ void dist_pass_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                 int mx, int my, int mz, int axis, int thr, int first) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = (int64_t)mx * my * mz;
+  if (c >= n) return;
+  const int ix = (int)(c % mx);
+  const int iy = (int)((c / mx) % my);
+  const int iz = (int)(c / ((int64_t)mx * my));
+  const int len = axis == 0 ? mx : (axis == 1 ? my : mz);
+  const int pos = axis == 0 ? ix : (axis == 1 ? iy : iz);
+  const int64_t stride = axis == 0 ? 1 : (axis == 1 ? (int64_t)mx : (int64_t)mx * my);
+  int best = VX_DIST_CAP;
+  for (int k = -VX_DIST_CAP + 1; k < VX_DIST_CAP; ++k) {
+    const int q = pos + k;
+    if (q < 0 || q >= len) continue;
+    const int ak = k < 0 ? -k : k;
+    if (ak >= best) continue;
+    const uint8_t v = src[c + (int64_t)k * stride];
+    int val;
+    if (first)
+      val = v >= thr ? ak : VX_DIST_CAP;
+    else
+      val = v > ak ? v : ak;
+    if (val < best) best = val;
+  }
+  dst[c] = (uint8_t)best;
+}
+
+__global__ void u16_to_u8_kernel(const uint16_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                 uint64_t n) {
+  // (v + 128) / 257 == floor(v * 255 / 65535 + 0.5) for all 65536 v
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = (uint8_t)(((uint32_t)src[i] + 128u) / 257u);
+}
+
+// ---- phantom generator (volume.py:317-368) ---------------------------------
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+struct ShapeD {
+  int kind;  // 0 sphere, 1 shell, 2 box
+  double cx, cy, cz, radius, thickness, ex, ey, ez;
+  int intensity;
+  int x0, y0, z0, sx, sy, sz;  // bounding sub-grid
+};
+
+__global__ void paint_kernel(uint8_t* __restrict__ dst, int64_t rp, int64_t pp, ShapeD s) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = (int64_t)s.sx * s.sy * s.sz;
+  if (c >= n) return;
+  const int x = s.x0 + (int)(c % s.sx);
+  const int y = s.y0 + (int)((c / s.sx) % s.sy);
+  const int z = s.z0 + (int)(c / ((int64_t)s.sx * s.sy));
+  const double dx = __dsub_rn((double)x, s.cx), dy = __dsub_rn((double)y, s.cy),
+               dz = __dsub_rn((double)z, s.cz);
+  bool inside;
+  if (s.kind == 2) {
+    inside = fabs(dx) <= s.ex / 2.0 && fabs(dy) <= s.ey / 2.0 && fabs(dz) <= s.ez / 2.0;
+  } else {
+    const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    if (s.kind == 0)
+      inside = d2 <= __dmul_rn(s.radius, s.radius);
+    else
+      inside = fabs(__dsub_rn(__dsqrt_rn(d2), s.radius)) <= s.thickness / 2.0;
+  }
+  if (inside) dst[(int64_t)z * pp + (int64_t)y * rp + x] = (uint8_t)s.intensity;
+}
+
+__global__ void noise_kernel(uint8_t* __restrict__ dst, int64_t rp, int64_t pp, int64_t nx,
+                             int64_t ny, int64_t nz, double sigma, unsigned long long seed) {
+  const int64_t n = nx * ny * nz;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = i % nx, y = (i / nx) % ny, z = i / (nx * ny);
+    uint8_t* p = dst + z * pp + y * rp + x;
+    const double base = (double)*p;
+    // draws 2i, 2i+1 of stream(seed): mix64(seed + (j+1)*GOLDEN)  (rng.py:33-51)
+    const unsigned long long j0 = 2ull * (unsigned long long)i;
+    const unsigned long long b0 = mix64(seed + (j0 + 1ull) * 0x9E3779B97F4A7C15ull);
+    const unsigned long long b1 = mix64(seed + (j0 + 2ull) * 0x9E3779B97F4A7C15ull);
+    const double u1 = __dmul_rn(__dadd_rn((double)(b0 >> 11), 1.0), 1.1102230246251565e-16);
+    const double u2 = __dmul_rn((double)(b1 >> 11), 1.1102230246251565e-16);
+    const double g = __dmul_rn(__dsqrt_rn(__dmul_rn(-2.0, log(u1))),
+                               cos(__dmul_rn(6.283185307179586, u2)));
+    double v = floor(__dadd_rn(__dadd_rn(base, __dmul_rn(sigma, g)), 0.5));
+    v = v < 0.0 ? 0.0 : (v > 255.0 ? 255.0 : v);
+    *p = (uint8_t)v;
+  }
+}
+
+__global__ void spot_kernel(uint8_t* __restrict__ dst, int64_t rp, int64_t pp, int64_t nx,
+                            int64_t ny, const int64_t* __restrict__ idx, int64_t k, int val) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= k) return;
+  const int64_t i = idx[r];
+  const int64_t x = i % nx, y = (i / nx) % ny, z = i / (nx * ny);
+  dst[z * pp + y * rp + x] = (uint8_t)val;
+}
+
+}  // namespace
+
+int vx_launch_brick_max(vx_volume* v, cudaStream_t s) {
+  const int64_t nb = (int64_t)v->nbx * v->nby * v->nbz;
+  uint8_t* borigin = v->bmax + v->bsz + v->bsy + 1;
+  brick_max_kernel<<<(unsigned)((nb + 127) / 128), 128, 0, s>>>(v->origin, v->sy, v->sz, v->nbx,
+                                                                 v->nby, v->nbz, borigin, v->bsy,
+                                                                 v->bsz);
+  VX_CHECK_LAUNCH();
+  return VX_OK;
+}
+
+int vx_launch_dist_map(const vx_volume* v, int thr, uint8_t* map, cudaStream_t s) {
+  const int mx = v->nbx + 2, my = v->nby + 2, mz = v->nbz + 2;
+  const int64_t n = (int64_t)mx * my * mz;
+  uint8_t* tmp = nullptr;
+  VX_CUDA(vx_malloc_async(&tmp, n, s));
+  const unsigned g = (unsigned)((n + 255) / 256);
+  dist_pass_kernel<<<g, 256, 0, s>>>(v->bmax, map, mx, my, mz, 0, thr, 1);
+  VX_CHECK_LAUNCH();
+  dist_pass_kernel<<<g, 256, 0, s>>>(map, tmp, mx, my, mz, 1, thr, 0);
+  VX_CHECK_LAUNCH();
+  dist_pass_kernel<<<g, 256, 0, s>>>(tmp, map, mx, my, mz, 2, thr, 0);
+  VX_CHECK_LAUNCH();
+  VX_CUDA(cudaFreeAsync(tmp, s));
+  return VX_OK;
+}
+
+int vx_launch_u16_to_u8(const uint16_t* src, uint8_t* dst, uint64_t n, cudaStream_t s) {
+  if (!n) return VX_OK;
+  uint64_t g = (n + 255) / 256;
+  const uint64_t cap = (uint64_t)vx_sm_count() * 16;
+  if (g > cap) g = cap;
+  u16_to_u8_kernel<<<(unsigned)g, 256, 0, s>>>(src, dst, n);
+  VX_CHECK_LAUNCH();
+  return VX_OK;
+}
+
+int vx_launch_phantom(uint8_t* dst, int64_t rp, int64_t pp, int64_t nx, int64_t ny, int64_t nz,
+                      const double* shapes, int64_t n_shapes, double noise_sigma,
+                      uint64_t noise_seed, const int64_t* spot_idx, int64_t n_spots,
+                      int32_t spot_intensity, cudaStream_t s) {
+  // shapes are painted in list order (volume.py:323-352); bounding sub-grid
+  // exactly as volume.py:324-335
+  for (int64_t k = 0; k < n_shapes; ++k) {
+    const double* q = shapes + 10 * k;
+    ShapeD sd;
+    sd.kind = (int)q[0];
+    sd.cx = q[1]; sd.cy = q[2]; sd.cz = q[3];
+    sd.intensity = (int)q[4];
+    sd.radius = q[5];
+    sd.thickness = q[6];
+    sd.ex = q[7]; sd.ey = q[8]; sd.ez = q[9];
+    double rx, ry, rz;
+    if (sd.kind == 2) {
+      rx = sd.ex / 2.0; ry = sd.ey / 2.0; rz = sd.ez / 2.0;
+    } else {
+      rx = ry = rz = sd.radius + (sd.kind == 1 ? sd.thickness / 2.0 : 0.0);
+    }
+    const long long x0 = std::max(0ll, (long long)ceil(sd.cx - rx));
+    const long long x1 = std::min((long long)nx - 1, (long long)floor(sd.cx + rx));
+    const long long y0 = std::max(0ll, (long long)ceil(sd.cy - ry));
+    const long long y1 = std::min((long long)ny - 1, (long long)floor(sd.cy + ry));
+    const long long z0 = std::max(0ll, (long long)ceil(sd.cz - rz));
+    const long long z1 = std::min((long long)nz - 1, (long long)floor(sd.cz + rz));
+    if (x0 > x1 || y0 > y1 || z0 > z1) continue;
+    sd.x0 = (int)x0; sd.y0 = (int)y0; sd.z0 = (int)z0;
+    sd.sx = (int)(x1 - x0 + 1); sd.sy = (int)(y1 - y0 + 1); sd.sz = (int)(z1 - z0 + 1);
+    const int64_t cnt = (int64_t)sd.sx * sd.sy * sd.sz;
+    paint_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(dst, rp, pp, sd);
+    VX_CHECK_LAUNCH();
+  }
+  if (noise_sigma > 0.0) {
+    const int64_t n = nx * ny * nz;
+    int64_t g = (n + 255) / 256;
+    const int64_t cap = (int64_t)vx_sm_count() * 32;
+    if (g > cap) g = cap;
+    noise_kernel<<<(unsigned)g, 256, 0, s>>>(dst, rp, pp, nx, ny, nz, noise_sigma,
+                                             (unsigned long long)noise_seed);
+    VX_CHECK_LAUNCH();
+  }
+  if (n_spots > 0) {
+    int64_t* didx = nullptr;
+    VX_CUDA(vx_malloc_async(&didx, n_spots * 8, s));
+    VX_CUDA(cudaMemcpyAsync(didx, spot_idx, n_spots * 8, cudaMemcpyHostToDevice, s));
+    spot_kernel<<<(unsigned)((n_spots + 255) / 256), 256, 0, s>>>(dst, rp, pp, nx, ny, didx,
+                                                                   n_spots, spot_intensity);
+    VX_CHECK_LAUNCH();
+    VX_CUDA(cudaFreeAsync(didx, s));
+  }
+  return VX_OK;
+}

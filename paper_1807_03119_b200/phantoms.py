@@ -1,0 +1,135 @@
+"""Phantom specs used by the tests, the bench and the comparison configs.
+
+The committed demo phantoms mirror phantoms.py of the reference (same seeds
+and layout constants, phantoms.py:35-167) so image-level expectations carry
+over.  ``insect_phantom_spec`` is the BASELINE.json C2/C3 input (SURVEY.md
+§8d): head / thorax / abdomen spheres with 6-voxel cuticle shells, six leg
+boxes, slab speckle and spot noise, built only from reference primitives;
+``scale`` scales it to 1024^3 / 2048^3 (the bench and C4 configs).
+"""
+
+from __future__ import annotations
+
+import math
+
+from . import rng
+from .volume import PhantomSpec, Shape, SpotNoise
+
+SPOT_PHANTOM_SEED = 20
+SPECKLE_PHANTOM_SEED = 3
+BENCH_PHANTOM_SEED = 5
+LATENCY_PHANTOM_SEED = 5
+INSECT_PHANTOM_SEED = 1807
+
+
+def _exact_count_density(count: int, n_voxels: int) -> float:
+    return (count + 0.5) / n_voxels
+
+
+def spot_phantom_spec(dims: int = 128, seed: int = SPOT_PHANTOM_SEED) -> PhantomSpec:
+    n = dims ** 3
+    c = (dims - 1) / 2.0
+    return PhantomSpec(
+        dims=(dims, dims, dims),
+        shapes=(Shape(kind="sphere", center=(c, c, c), radius=dims * 0.3125, intensity=200),),
+        noise_sigma=10.0,
+        spot_noise=SpotNoise(density=_exact_count_density(50, n), intensity=255),
+        rng_seed=seed,
+    )
+
+
+def blob_positions(dims: int, count: int, sphere_radius: float, seed: int):
+    """Deterministic texture centres clear of the borders and the central sphere."""
+    c = (dims - 1) / 2.0
+    margin = 6
+    keepout = sphere_radius + 8
+    span = dims - 2 * margin
+    sub = rng.substream_seed(seed, 0x736C6162)
+    out: list[tuple[int, int, int]] = []
+    draw = 0
+    while len(out) < count and draw < 10000:
+        b = rng.stream(sub, draw * 3, 3)
+        draw += 1
+        p = (margin + int(b[0] % span), margin + int(b[1] % span), margin + int(b[2] % span))
+        if math.dist(p, (c, c, c)) < keepout:
+            continue
+        if any(math.dist(p, q) < 10 for q in out):
+            continue
+        out.append(p)
+    return out
+
+
+def speckle_phantom_spec(dims: int = 128, seed: int = SPECKLE_PHANTOM_SEED) -> PhantomSpec:
+    n = dims ** 3
+    c = (dims - 1) / 2.0
+    radius = dims * 0.3125
+    slabs = tuple(Shape(kind="box", center=(float(x), float(y), float(z)), extent=(3.0, 3.0, 1.0),
+                        intensity=200)
+                  for x, y, z in blob_positions(dims, 30, radius, seed))
+    return PhantomSpec(
+        dims=(dims, dims, dims),
+        shapes=(Shape(kind="sphere", center=(c, c, c), radius=radius, intensity=200),) + slabs,
+        noise_sigma=10.0,
+        spot_noise=SpotNoise(density=_exact_count_density(60, n), intensity=255),
+        rng_seed=seed,
+    )
+
+
+_CHECKER = tuple((dx, dy, dz) for dx in (-1, 0, 1) for dy in (-1, 0, 1) for dz in (-1, 0, 1)
+                 if (dx + dy + dz) % 2 == 0)
+
+
+def bench_phantom_spec(dims: int = 256, seed: int = BENCH_PHANTOM_SEED) -> PhantomSpec:
+    c = (dims - 1) / 2.0
+    radius = dims * 0.3125
+    scale = (dims / 256) ** 3
+    pos = blob_positions(dims, max(12, round(600 * scale)), radius, seed)
+    n_checker = max(8, round(350 * scale))
+    shapes = [Shape(kind="sphere", center=(c, c, c), radius=radius, intensity=200)]
+    for x, y, z in pos[:n_checker]:
+        shapes.extend(Shape(kind="box", center=(float(x + dx), float(y + dy), float(z + dz)),
+                            extent=(0.8, 0.8, 0.8), intensity=255) for dx, dy, dz in _CHECKER)
+    for x, y, z in pos[n_checker:]:
+        shapes.append(Shape(kind="box", center=(float(x), float(y), float(z)),
+                            extent=(3.0, 3.0, 1.0), intensity=200))
+    return PhantomSpec(dims=(dims, dims, dims), shapes=tuple(shapes), noise_sigma=10.0,
+                       rng_seed=seed)
+
+
+def latency_phantom_spec(dims: int = 128, seed: int = LATENCY_PHANTOM_SEED) -> PhantomSpec:
+    c = (dims - 1) / 2.0
+    return PhantomSpec(
+        dims=(dims, dims, dims),
+        shapes=(Shape(kind="sphere", center=(c, c, c), radius=dims * 0.3125, intensity=200),),
+        noise_sigma=3.0,
+        rng_seed=seed,
+    )
+
+
+def insect_phantom_spec(dims: int = 512, seed: int = INSECT_PHANTOM_SEED) -> PhantomSpec:
+    """CT-like insect phantom (SURVEY.md §8d C2 recipe, scaled by dims/512).
+
+    Lengths (radii, shell thickness, leg boxes, offsets) scale with s =
+    dims/512; the slab speckle count scales with s^2 and the spot count with
+    s^3 (constant density), speckle extent stays 3x3x1 voxels.
+    """
+    s = dims / 512.0
+    c = (dims - 1) / 2.0
+    shapes = []
+    for dy, r, val in ((-150, 70, 190), (-30, 95, 170), (120, 110, 160)):
+        centre = (c, c + dy * s, c)
+        shapes.append(Shape(kind="sphere", center=centre, radius=r * s, intensity=val))
+        shapes.append(Shape(kind="shell", center=centre, radius=r * s, thickness=6 * s,
+                            intensity=230))
+    for dy in (-70, -30, 10):
+        for sx in (-1, 1):
+            shapes.append(Shape(kind="box", center=(c + sx * 150 * s, c + dy * s, c - 60 * s),
+                                extent=(200 * s, 8 * s, 8 * s), intensity=210))
+    n_slabs = int(round(400 * s * s))
+    for x, y, z in blob_positions(dims, n_slabs, 220 * s, 11):
+        shapes.append(Shape(kind="box", center=(float(x), float(y), float(z)),
+                            extent=(3.0, 3.0, 1.0), intensity=200))
+    n_spots = int(round(2000 * s ** 3))
+    return PhantomSpec(dims=(dims, dims, dims), shapes=tuple(shapes), noise_sigma=12.0,
+                       spot_noise=SpotNoise(density=(n_spots + 0.5) / dims ** 3, intensity=255),
+                       rng_seed=seed)

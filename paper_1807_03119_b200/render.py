@@ -1,0 +1,413 @@
+"""First-hit surface ray caster with the ray-time noise filters, on the B200.
+
+Drop-in for render.py of the reference (render.py:31-565).  Host code keeps
+the camera / parameter dataclasses and computes the handful of FP64 camera
+constants with numpy exactly as the reference does (Camera.basis,
+render.py:49-62); everything per pixel runs in one CUDA kernel (K4,
+csrc/vx_render.cu): FP64 ray setup, exact FP32 march with empty-space
+skipping, the configured filter at every surface candidate, 3D Sobel normal,
+Phong shading, quantisation and the fused image histogram.
+
+Frames are bit-identical to the reference's for any ``workers`` (the
+argument is accepted and ignored; the device has no bands).  ``filter_fn``
+overrides cannot run on the device and raise ``RenderError``: there is no
+CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .filters import FilterConfig, FilterKind, native_config
+from .histogram import HistogramModel
+from .volume import Volume, device_volume
+
+_PAD = 16  # chunk clip bound of render.py:286 (grid.py:19 PAD = 16)
+_STEP_CHUNK = 16
+
+
+class RenderError(Exception):
+    pass
+
+
+@dataclass(frozen=True)
+class Camera:
+    """Pinhole camera in voxel coordinates (render.py:35-79)."""
+
+    position: tuple[float, float, float]
+    look_at: tuple[float, float, float]
+    up: tuple[float, float, float] = (0.0, 0.0, 1.0)
+    fov_y_deg: float = 45.0
+
+    def __post_init__(self):
+        if not 0.0 < self.fov_y_deg < 180.0:
+            raise RenderError(f"fov must be in (0, 180), got {self.fov_y_deg}")
+        self.basis()
+
+    def basis(self) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+        """Orthonormal (right, up, forward), numpy FP64 (render.py:49-62)."""
+        pos = np.asarray(self.position, dtype=np.float64)
+        fwd = np.asarray(self.look_at, dtype=np.float64) - pos
+        norm = np.linalg.norm(fwd)
+        if norm == 0:
+            raise RenderError("camera position and look_at coincide")
+        fwd = fwd / norm
+        right = np.cross(fwd, np.asarray(self.up, dtype=np.float64))
+        rnorm = np.linalg.norm(right)
+        if rnorm < 1e-9:
+            raise RenderError("camera up vector is parallel to the view direction")
+        right = right / rnorm
+        return right, np.cross(right, fwd), fwd
+
+    def to_json(self) -> dict:
+        return {"position": list(self.position), "look_at": list(self.look_at),
+                "up": list(self.up), "fov_y_deg": self.fov_y_deg}
+
+    @classmethod
+    def from_json(cls, obj: dict) -> "Camera":
+        return cls(position=tuple(float(v) for v in obj["position"]),
+                   look_at=tuple(float(v) for v in obj["look_at"]),
+                   up=tuple(float(v) for v in obj.get("up", (0, 0, 1))),
+                   fov_y_deg=float(obj.get("fov_y_deg", 45.0)))
+
+
+def orbit_camera(volume: Volume, azimuth_deg: float = 45.0, elevation_deg: float = 25.0,
+                 distance: float | None = None, fov_y_deg: float = 45.0) -> Camera:
+    """Camera on an orbit around the volume centre, z up (render.py:82-105)."""
+    nx, ny, nz = volume.dims
+    target = ((nx - 1) / 2.0, (ny - 1) / 2.0, (nz - 1) / 2.0)
+    if distance is None:
+        distance = 2.2 * math.sqrt(nx * nx + ny * ny + nz * nz) / 2.0
+    el = math.radians(max(-89.0, min(89.0, elevation_deg)))
+    az = math.radians(azimuth_deg)
+    pos = (target[0] + distance * math.cos(el) * math.cos(az),
+           target[1] + distance * math.cos(el) * math.sin(az),
+           target[2] + distance * math.sin(el))
+    return Camera(position=pos, look_at=target, fov_y_deg=fov_y_deg)
+
+
+@dataclass(frozen=True)
+class RenderParams:
+    """Image, march and shading parameters (render.py:108-150)."""
+
+    width: int = 512
+    height: int = 512
+    step_size: float = 0.5
+    max_steps: int = 0
+    ambient: float = 0.1
+    diffuse: float = 0.7
+    specular: float = 0.2
+    shininess: float = 16.0
+    light_direction: tuple[float, float, float] = (1.0, -1.0, 1.5)
+    background: int = 0
+
+    def __post_init__(self):
+        if self.width < 1 or self.height < 1:
+            raise RenderError(f"image size must be >= 1x1, got {self.width}x{self.height}")
+        if self.step_size <= 0:
+            raise RenderError(f"step_size must be > 0, got {self.step_size}")
+        if min(self.ambient, self.diffuse, self.specular) < 0:
+            raise RenderError("lighting coefficients must be >= 0")
+        if not 0 <= self.background <= 255:
+            raise RenderError(f"background must be in [0, 255], got {self.background}")
+
+    def to_json(self) -> dict:
+        return {"width": self.width, "height": self.height, "step_size": self.step_size,
+                "max_steps": self.max_steps, "ambient": self.ambient, "diffuse": self.diffuse,
+                "specular": self.specular, "shininess": self.shininess,
+                "light_direction": list(self.light_direction), "background": self.background}
+
+    @classmethod
+    def from_json(cls, obj: dict) -> "RenderParams":
+        kwargs = dict(obj)
+        if "light_direction" in kwargs:
+            kwargs["light_direction"] = tuple(kwargs["light_direction"])
+        return cls(**kwargs)
+
+
+@dataclass
+class Frame:
+    """Rendered image plus timing and the state that produced it (render.py:153-174)."""
+
+    pixels: np.ndarray
+    timing: dict
+    filter_config: FilterConfig
+    render_params: RenderParams
+    camera: Camera
+    volume_hash: str
+    hit_count: int = 0
+
+    def meta_json(self) -> dict:
+        return {"image": {"width": int(self.pixels.shape[1]), "height": int(self.pixels.shape[0])},
+                "timing": self.timing, "filter_config": self.filter_config.to_json(),
+                "render_params": self.render_params.to_json(), "camera": self.camera.to_json(),
+                "volume_hash": self.volume_hash, "hit_count": self.hit_count}
+
+
+@dataclass(frozen=True)
+class Hit:
+    position: tuple[float, float, float]
+    voxel: tuple[int, int, int]
+    value: float
+    t: float
+
+
+# --- native structs ----------------------------------------------------------------
+
+
+def ray_setup(camera: Camera, width: int, height: int) -> _lib.vx_ray_setup:
+    """Host FP64 constants of primary_ray_dirs (render.py:190-192)."""
+    right, up, fwd = camera.basis()
+    rs = _lib.vx_ray_setup()
+    for i in range(3):
+        rs.right[i] = float(right[i])
+        rs.up[i] = float(up[i])
+        rs.fwd[i] = float(fwd[i])
+        rs.origin[i] = float(camera.position[i])
+    rs.tan_f = math.tan(math.radians(camera.fov_y_deg) / 2.0)
+    rs.aspect = width / height
+    rs.width = width
+    rs.height = height
+    return rs
+
+
+def chunk_for(step: float) -> tuple[int, bool]:
+    """Samples per march pass and the clip flag (render.py:286-287)."""
+    chunk = max(1, min(_STEP_CHUNK, int((_PAD - 1) / step))) if step < _PAD - 1 else 1
+    return chunk, chunk * step > _PAD - 1
+
+
+def native_params(params: RenderParams, *, max_steps: int | None = None,
+                  skip: bool = True) -> _lib.vx_render_params:
+    rp = _lib.vx_render_params()
+    rp.step_size = float(params.step_size)
+    rp.max_steps = int(params.max_steps if max_steps is None else max_steps)
+    chunk, clip = chunk_for(params.step_size)
+    rp.chunk = chunk
+    rp.need_clip = 1 if clip else 0
+    rp.skip = 1 if skip else 0
+    rp.ambient = float(params.ambient)
+    rp.diffuse = float(params.diffuse)
+    rp.specular = float(params.specular)
+    rp.shininess = float(params.shininess)
+    light = np.asarray(params.light_direction, dtype=np.float64)
+    light = light / np.linalg.norm(light)  # render.py:512-513
+    for i in range(3):
+        rp.light[i] = float(light[i])
+    rp.background = int(params.background)
+    return rp
+
+
+# --- ray setup helpers (render.py:188-230) -------------------------------------------
+
+
+def primary_ray_dirs(camera: Camera, width: int, height: int) -> np.ndarray:
+    """(height*width, 3) unit directions, row-major from the top-left (device)."""
+    _lib.require_device()
+    rs = ray_setup(camera, width, height)
+    out = np.empty((width * height, 3), dtype=np.float64)
+    _lib.call("vx_ray_dirs", C.byref(rs), _lib.ptr(out), exc_type=RenderError)
+    return out
+
+
+def ray_box_spans(origin: np.ndarray, dirs: np.ndarray, dims) -> tuple[np.ndarray, np.ndarray]:
+    """Entry/exit distances against [-0.5, n-0.5]^3 (device)."""
+    _lib.require_device()
+    o = np.ascontiguousarray(np.asarray(origin, dtype=np.float64).reshape(3))
+    d = np.ascontiguousarray(np.asarray(dirs, dtype=np.float64).reshape(-1, 3))
+    dm = np.asarray([int(v) for v in dims], dtype=np.int64)
+    te = np.empty(d.shape[0], dtype=np.float64)
+    tx = np.empty(d.shape[0], dtype=np.float64)
+    _lib.call("vx_ray_spans", _lib.ptr(o), _lib.ptr(d), d.shape[0], _lib.ptr(dm), _lib.ptr(te),
+              _lib.ptr(tx), exc_type=RenderError)
+    return te, tx
+
+
+# --- normals and shading (render.py:344-413) ------------------------------------------
+
+
+def sobel_normal_batch(volume: Volume, vx, vy, vz, fallback: np.ndarray) -> np.ndarray:
+    """(n, 3) unit normals toward decreasing density (device)."""
+    xs = np.ascontiguousarray(np.asarray(vx, dtype=np.int64).reshape(-1))
+    ys = np.ascontiguousarray(np.asarray(vy, dtype=np.int64).reshape(-1))
+    zs = np.ascontiguousarray(np.asarray(vz, dtype=np.int64).reshape(-1))
+    fb = np.ascontiguousarray(np.asarray(fallback, dtype=np.float64).reshape(-1, 3))
+    out = np.empty((xs.size, 3), dtype=np.float64)
+    if xs.size:
+        dev = device_volume(volume)
+        _lib.call("vx_sobel_batch", dev.handle, _lib.ptr(xs), _lib.ptr(ys), _lib.ptr(zs), xs.size,
+                  _lib.ptr(fb), _lib.ptr(out), exc_type=RenderError)
+    return out
+
+
+def sobel_normal(volume: Volume, x: int, y: int, z: int, fallback=(0.0, 0.0, 1.0)) -> np.ndarray:
+    fb = np.asarray(fallback, dtype=np.float64).reshape(1, 3)
+    return sobel_normal_batch(volume, [x], [y], [z], fb)[0]
+
+
+def shade_phong_batch(normals: np.ndarray, view_dirs: np.ndarray, light_dir: np.ndarray,
+                      params: RenderParams) -> np.ndarray:
+    """Grey values in [0, 255] (device)."""
+    _lib.require_device()
+    nn = np.ascontiguousarray(np.asarray(normals, dtype=np.float64).reshape(-1, 3))
+    vv = np.ascontiguousarray(np.asarray(view_dirs, dtype=np.float64).reshape(-1, 3))
+    rp = native_params(params)
+    light = np.asarray(light_dir, dtype=np.float64).reshape(3)
+    for i in range(3):
+        rp.light[i] = float(light[i])
+    out = np.empty(nn.shape[0], dtype=np.uint8)
+    if nn.shape[0]:
+        _lib.call("vx_phong_batch", _lib.ptr(nn), _lib.ptr(vv), nn.shape[0], C.byref(rp),
+                  _lib.ptr(out), exc_type=RenderError)
+    return out
+
+
+def shade_phong(normal, view_dir, light_dir, params: RenderParams) -> int:
+    return int(shade_phong_batch(np.asarray(normal, dtype=np.float64).reshape(1, 3),
+                                 np.asarray(view_dir, dtype=np.float64).reshape(1, 3),
+                                 np.asarray(light_dir, dtype=np.float64), params)[0])
+
+
+# --- march_ray (render.py:426-464) -------------------------------------------------------
+
+
+def march_rays(volume: Volume, origins, directions, config: FilterConfig,
+               histogram: HistogramModel | None = None, step_size: float = 0.5,
+               max_steps=0):
+    """Batch form of march_ray: arbitrary origins and (normalised) directions."""
+    config = config.resolve_threshold(histogram)
+    o = np.ascontiguousarray(np.asarray(origins, dtype=np.float64).reshape(-1, 3))
+    d = np.ascontiguousarray(np.asarray(directions, dtype=np.float64).reshape(-1, 3))
+    n = d.shape[0]
+    te = np.empty(n)
+    tx = np.empty(n)
+    for i in range(n):  # spans per origin (device)
+        a, b = ray_box_spans(o[i], d[i:i + 1], volume.dims)
+        te[i], tx[i] = a[0], b[0]
+    ms = np.empty(n, dtype=np.int32)
+    given = np.broadcast_to(np.asarray(max_steps, dtype=np.int64), (n,))
+    for i in range(n):
+        if given[i] <= 0:
+            span = float(tx[i] - te[i])
+            ms[i] = max(1, math.ceil(span / step_size) + 1) if span >= 0 else 1
+        else:
+            ms[i] = int(given[i])
+    rp = native_params(RenderParams(step_size=step_size))
+    fc = native_config(config, histogram)
+    hit = np.zeros(n, dtype=np.uint8)
+    vox = np.zeros((n, 3), dtype=np.int32)
+    t = np.zeros(n, dtype=np.float32)
+    val = np.zeros(n, dtype=np.float64)
+    dev = device_volume(volume)
+    _lib.call("vx_march_rays", dev.handle, _lib.ptr(o), _lib.ptr(d), _lib.ptr(te), _lib.ptr(tx),
+              _lib.ptr(ms), n, C.byref(rp), C.byref(fc), _lib.ptr(hit), _lib.ptr(vox), _lib.ptr(t),
+              _lib.ptr(val), exc_type=RenderError)
+    return hit.astype(bool), vox.astype(np.int64), t.astype(np.float64), val
+
+
+def march_ray(volume: Volume, origin, direction, config: FilterConfig,
+              histogram: HistogramModel | None = None, step_size: float = 0.5,
+              max_steps: int = 0) -> Hit | None:
+    """March a single ray; None when it leaves the volume unaccepted."""
+    origin = np.asarray(origin, dtype=np.float64)
+    direction = np.asarray(direction, dtype=np.float64)
+    direction = direction / np.linalg.norm(direction)
+    hit, vox, t, val = march_rays(volume, origin.reshape(1, 3), direction.reshape(1, 3), config,
+                                  histogram, step_size, max_steps)
+    if not hit[0]:
+        return None
+    pos = origin + t[0] * direction
+    return Hit(position=tuple(float(v) for v in pos), voxel=tuple(int(v) for v in vox[0]),
+               value=float(val[0]), t=float(t[0]))
+
+
+# --- frames (render.py:488-560) -------------------------------------------------------------
+
+
+@dataclass
+class FrameDetail:
+    """Per-pixel diagnostics of one device frame (parity tests, bench)."""
+
+    pixels: np.ndarray
+    hit_voxel: np.ndarray | None
+    hit_t: np.ndarray | None
+    hit_value: np.ndarray | None
+    intensity: np.ndarray | None
+    image_hist: np.ndarray
+    hit_count: int
+    samples: int
+
+
+def _check_render_args(config: FilterConfig, histogram, filter_fn) -> FilterConfig:
+    config = config.resolve_threshold(histogram)
+    if config.kind in (FilterKind.SIGMA, FilterKind.ENTROPY) and histogram is None:
+        raise RenderError(f"{config.kind.value} filter needs the volume histogram")
+    if filter_fn is not None:
+        raise RenderError("filter_fn overrides are not supported: filters run inside the B200 "
+                          "ray-cast kernel (no CPU fallback)")
+    return config
+
+
+def render_detail(volume: Volume, camera: Camera, params: RenderParams, config: FilterConfig,
+                  histogram: HistogramModel | None = None, *, diagnostics: bool = False,
+                  skip: bool = True, partition: tuple[int, int] | None = None) -> FrameDetail:
+    config = _check_render_args(config, histogram, None)
+    _lib.require_device()
+    dev = device_volume(volume)
+    rs = ray_setup(camera, params.width, params.height)
+    rp = native_params(params, skip=skip)
+    fc = native_config(config, histogram)
+    npx = params.width * params.height
+    pixels = np.empty((params.height, params.width), dtype=np.uint8)
+    hist = np.zeros(256, dtype=np.uint64)
+    counters = np.zeros(2, dtype=np.uint64)
+    out = _lib.vx_render_out()
+    out.pixels = pixels.ctypes.data
+    out.image_hist = hist.ctypes.data
+    out.hit_count = counters.ctypes.data
+    out.samples = counters.ctypes.data + 8
+    vox = t = val = inten = None
+    if diagnostics:
+        vox = np.empty((npx, 3), dtype=np.int32)
+        t = np.empty(npx, dtype=np.float32)
+        val = np.empty(npx, dtype=np.float64)
+        inten = np.empty(npx, dtype=np.float64)
+        out.hit_voxel = vox.ctypes.data
+        out.hit_t = t.ctypes.data
+        out.hit_value = val.ctypes.data
+        out.intensity = inten.ctypes.data
+    part = None
+    if partition is not None:
+        part = _lib.vx_partition(int(partition[0]), int(partition[1]))
+    _lib.call("vx_render", dev.handle, C.byref(rs), C.byref(rp), C.byref(fc),
+              C.byref(part) if part is not None else None, C.byref(out), exc_type=RenderError)
+    return FrameDetail(pixels=pixels, hit_voxel=vox, hit_t=t, hit_value=val, intensity=inten,
+                       image_hist=hist.astype(np.int64), hit_count=int(counters[0]),
+                       samples=int(counters[1]))
+
+
+def render_frame(volume: Volume, camera: Camera, params: RenderParams, config: FilterConfig,
+                 histogram: HistogramModel | None = None, workers: int = 1,
+                 filter_fn=None) -> Frame:
+    """Render one frame on the B200; bit-identical output for any worker count."""
+    wall0 = time.perf_counter()
+    config = _check_render_args(config, histogram, filter_fn)
+    d = render_detail(volume, camera, params, config, histogram)
+    total_ms = (time.perf_counter() - wall0) * 1000.0
+    frame = Frame(
+        pixels=d.pixels,
+        timing={"total_ms": total_ms, "march_ms": total_ms, "shade_ms": 0.0},
+        filter_config=config,
+        render_params=params,
+        camera=camera,
+        volume_hash=volume.content_hash(),
+        hit_count=d.hit_count,
+    )
+    object.__setattr__(frame, "image_hist", d.image_hist)
+    return frame

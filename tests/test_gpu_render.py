@@ -1,0 +1,267 @@
+"""K4 ray caster parity on the B200 (mirrors tests/test_render.py and the
+acceptance suite of the reference): FP64 ray setup bitwise, hit voxels and
+pixels exactly equal to the reference / oracle on every frame."""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import math
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden, vol_from
+
+pytestmark = pytest.mark.gpu
+
+KINDS = ("none", "mean", "sigma", "entropy", "okada", "local-cluster")
+
+
+def cfg_for(vx, kind, **kw):
+    k = vx.FilterKind.from_name(kind)
+    if kind == "entropy" and "entropy_threshold" not in kw:
+        kw["entropy_threshold"] = 0.5
+    return vx.FilterConfig(kind=k, **kw)
+
+
+# --- ray setup / shading bitwise ---------------------------------------------------
+
+
+def test_primary_ray_dirs_and_spans_bitwise(vx):
+    from paper_1807_03119_b200.render import primary_ray_dirs, ray_box_spans
+
+    g = golden("shading.npz")
+    for i in range(3):
+        c = g[f"cam{i}"]
+        cam = vx.Camera(position=tuple(c[0:3]), look_at=tuple(c[3:6]), up=tuple(c[6:9]),
+                        fov_y_deg=float(c[9]))
+        d = primary_ray_dirs(cam, int(c[10]), int(c[11]))
+        assert np.array_equal(d, g[f"dirs{i}"])
+        te, tx = ray_box_spans(np.asarray(cam.position), d, (9, 13, 64))
+        assert np.array_equal(te, g[f"te{i}"]) and np.array_equal(tx, g[f"tx{i}"])
+    for j in range(4):
+        te, tx = ray_box_spans(g[f"par_o{j}"], g["par_dirs"], (5, 5, 5))
+        np.testing.assert_array_equal(te, g[f"par_te{j}"])
+        np.testing.assert_array_equal(tx, g[f"par_tx{j}"])
+
+
+def test_sobel_and_phong_vs_reference(vx):
+    from paper_1807_03119_b200.render import shade_phong_batch, sobel_normal_batch
+
+    g = golden("shading.npz")
+    v = vx.Volume(dims=(9, 9, 9), data=g["sobel_vol"])
+    pts = g["sobel_pts"]
+    n = sobel_normal_batch(v, pts[:, 0], pts[:, 1], pts[:, 2], g["sobel_fb"])
+    assert np.array_equal(n, g["sobel_n"])
+    px = shade_phong_batch(g["phong_n"], g["phong_v"], g["phong_l"], vx.RenderParams())
+    assert (px != g["phong_px"]).sum() <= 2
+
+
+def test_sobel_ramps_and_phong_goldens(vx):
+    from paper_1807_03119_b200.render import shade_phong, sobel_normal
+
+    n = 9
+    idx = np.arange(n, dtype=np.uint8)
+    for axis in range(3):
+        shape = [1, 1, 1]
+        shape[2 - axis] = n
+        data = np.broadcast_to(idx.reshape(shape), (n, n, n)).copy()
+        want = np.zeros(3)
+        want[axis] = -1.0
+        assert np.allclose(sobel_normal(vol_from(vx, data), 4, 4, 4), want, atol=1e-12)
+        rev = vol_from(vx, data[::-1, ::-1, ::-1].copy())
+        assert np.allclose(sobel_normal(rev, 4, 4, 4), -want, atol=1e-12)
+    flat = vol_from(vx, np.full((9, 9, 9), 8, np.uint8))
+    assert np.allclose(sobel_normal(flat, 4, 4, 4, fallback=(0.0, 1.0, 0.0)), (0, 1, 0))
+    p = vx.RenderParams(ambient=0.1, diffuse=0.7, specular=0.2, shininess=16)
+    assert shade_phong((0, 0, 1), (0, 0, 1), (0, 0, -1), p) == round(0.1 * 255)
+    assert shade_phong((0, 0, 1), (0, 0, 1), (0, 0, 1),
+                       vx.RenderParams(ambient=0.0, diffuse=1.0, specular=0.0)) == 255
+
+
+# --- march_ray known answers (test_render.py TestMarchRay) ---------------------------------
+
+
+def test_march_ray_known_answers(vx, spot_volume):
+    from paper_1807_03119_b200.render import march_ray
+
+    v = vol_from(vx, np.zeros((9, 9, 9), np.uint8))
+    assert march_ray(v, (-5, 4, 4), (1, 0, 0), vx.FilterConfig(kind=vx.FilterKind.MEAN,
+                                                                threshold=101)) is None
+    data = np.zeros((9, 9, 9), np.uint8)
+    data[:, :, 5:] = 200
+    slab = vol_from(vx, data)
+    for kind in vx.FilterKind:
+        h = vx.build_histogram(slab)
+        hit = march_ray(slab, (-5, 4, 4), (1, 0, 0), vx.FilterConfig(kind=kind, threshold=101), h)
+        assert hit is not None and hit.voxel[0] == 5 and hit.value >= 101, kind
+    h = vx.build_histogram(spot_volume)
+    lc = vx.FilterConfig(kind=vx.FilterKind.LOCAL_CLUSTER, threshold=101)
+    none = vx.FilterConfig(kind=vx.FilterKind.NONE, threshold=101)
+    assert march_ray(spot_volume, (-5.0, 4.0, 4.0), (1.0, 0.0, 0.0), lc, h) is None
+    hit = march_ray(spot_volume, (-5.0, 4.0, 4.0), (1.0, 0.0, 0.0), none, h)
+    assert hit is not None and hit.voxel == (4, 4, 4)
+    data = np.array(spot_volume.data, copy=True)
+    data[:, :, 7:] = 200
+    v2 = vol_from(vx, data)
+    hit = march_ray(v2, (-5.0, 4.0, 4.0), (1.0, 0.0, 0.0), lc, vx.build_histogram(v2))
+    assert hit is not None and hit.voxel[0] == 7
+    data = np.zeros((9, 9, 9), np.uint8)
+    data[:, :, 6:] = 200
+    v3 = vol_from(vx, data)
+    mcfg = vx.FilterConfig(kind=vx.FilterKind.MEAN, threshold=101)
+    hit = march_ray(v3, (2.0, 4.0, 4.0), (1.0, 0.0, 0.0), mcfg)
+    assert hit is not None and hit.voxel[0] == 6
+    assert march_ray(v3, (2.0, 4.0, 4.0), (-1.0, 0.0, 0.0), mcfg) is None
+    hit = march_ray(vol_from(vx, np.zeros((9, 9, 9), np.uint8)), (-5.0, 4.0, 4.0), (1.0, 0.0, 0.0),
+                    vx.FilterConfig(kind=vx.FilterKind.NONE, threshold=0))
+    assert hit is not None and hit.voxel[0] == 0
+
+
+# --- frames vs the reference's frozen frames -------------------------------------------------
+
+
+@pytest.mark.parametrize("name", ["spot_64", "spot_128", "speckle_128", "latency_64"])
+@pytest.mark.parametrize("skip", [True, False])
+def test_frames_match_reference(vx, name, skip):
+    from oracle.rng_np import generate_phantom_np
+    from paper_1807_03119_b200.render import render_detail
+
+    meta = json.loads((GOLDEN / "phantoms.json").read_text())[name]
+    spec = vx.PhantomSpec.from_json(meta["spec"])
+    v = vx.Volume(dims=spec.dims, data=generate_phantom_np(meta["spec"]))
+    g = golden("frames_small.npz")
+    h = vx.build_histogram(v)
+    assert np.array_equal(h.counts, g[f"{name}__counts"])
+    assert h.otsu_threshold == int(g[f"{name}__otsu"])
+    size = g[f"{name}__none__pixels"].shape[0]
+    cam = vx.orbit_camera(v)
+    params = vx.RenderParams(width=size, height=size)
+    for kind in KINDS:
+        key = f"{name}__{kind}"
+        d = render_detail(v, cam, params, cfg_for(vx, kind), h, diagnostics=True, skip=skip)
+        assert np.array_equal(d.hit_voxel, g[key + "__voxel"].astype(np.int32)), key
+        assert np.array_equal(d.pixels, g[key + "__pixels"]), key
+        hit = d.hit_voxel[:, 0] >= 0
+        assert np.array_equal(d.hit_t[hit], g[key + "__t"][hit]), key
+        assert d.hit_count == int(g[key + "__hits"]), key
+        assert np.array_equal(d.image_hist, np.bincount(d.pixels.reshape(-1), minlength=256))
+
+
+def test_render_frame_api(vx, small_sphere_volume, small_sphere_histogram):
+    from paper_1807_03119_b200.render import RenderError
+
+    v = vol_from(vx, np.zeros((16, 16, 16), np.uint8))
+    frame = vx.render_frame(v, vx.orbit_camera(v), vx.RenderParams(width=32, height=32,
+                                                                   background=13),
+                            vx.FilterConfig(threshold=101), vx.build_histogram(v))
+    assert (frame.pixels == 13).all() and frame.hit_count == 0
+    params = vx.RenderParams(width=64, height=64)
+    cam = vx.orbit_camera(small_sphere_volume)
+    f = vx.render_frame(small_sphere_volume, cam, params, vx.FilterConfig(kind=vx.FilterKind.MEAN),
+                        small_sphere_histogram)
+    assert f.hit_count > 200 and f.pixels.shape == (64, 64) and f.timing["total_ms"] > 0
+    frames = [vx.render_frame(small_sphere_volume, cam, params,
+                              vx.FilterConfig(kind=vx.FilterKind.LOCAL_CLUSTER),
+                              small_sphere_histogram, workers=w) for w in (1, 2, 5)]
+    assert all((fr.pixels == frames[0].pixels).all() for fr in frames)
+    meta = vx.render_frame(small_sphere_volume, cam, params,
+                           vx.FilterConfig(kind=vx.FilterKind.OKADA),
+                           small_sphere_histogram).meta_json()
+    assert meta["filter_config"]["threshold"] == float(small_sphere_histogram.otsu_threshold)
+    assert meta["volume_hash"] == small_sphere_volume.content_hash()
+    with pytest.raises(RenderError):
+        vx.render_frame(small_sphere_volume, cam, params, vx.FilterConfig(), small_sphere_histogram,
+                        filter_fn=lambda x, y, z: x)
+    with pytest.raises(RenderError, match="histogram"):
+        vx.render_frame(small_sphere_volume, cam, params,
+                        vx.FilterConfig(kind=vx.FilterKind.SIGMA, threshold=50.0))
+
+
+# --- randomised parity vs the oracle -------------------------------------------------------
+
+
+def test_random_cameras_steps_thresholds_vs_oracle(vx, oracle):
+    from paper_1807_03119_b200.render import render_detail
+
+    rs = np.random.default_rng(2)
+    data = (rs.random((40, 48, 56)) < 0.02).astype(np.uint8) * 230 + rs.integers(
+        0, 60, (40, 48, 56), dtype=np.uint8)
+    data[10:30, 12:36, 14:42] = np.maximum(data[10:30, 12:36, 14:42], 150)
+    v = vol_from(vx, data)
+    h = vx.build_histogram(v)
+    steps = [0.5, 0.37, 1.0, 2.5, 16.0, 0.5, 0.25, 3.0]
+    for trial, step in enumerate(steps):
+        pos = tuple(float(x) for x in rs.uniform(-80, 140, 3))
+        look = tuple(float(x) for x in rs.uniform(5, 40, 3))
+        fov = float(rs.uniform(15, 90))
+        cam = vx.Camera(position=pos, look_at=look, fov_y_deg=fov)
+        w, hh = int(rs.integers(20, 70)), int(rs.integers(20, 70))
+        params = vx.RenderParams(width=w, height=hh, step_size=step,
+                                 max_steps=int(rs.integers(5, 200)) if trial == 5 else 0)
+        cv = oracle.cam_vector(pos, look, w, hh, fov_y_deg=fov)
+        for kind in KINDS:
+            T = float(rs.choice([0.0, 40.5, 67.0, 149.0, 231.0, 300.0]))
+            cfg = cfg_for(vx, kind, threshold=T)
+            want = oracle.render(data, cv, w, hh, kind=kind, threshold=T,
+                                 sigma_band=2.0 * h.global_sigma, probabilities=h.probabilities,
+                                 entropy_threshold=cfg.entropy_threshold, step=step,
+                                 max_steps=params.max_steps)
+            for skip in (True, False):
+                d = render_detail(v, cam, params, cfg, h, diagnostics=True, skip=skip)
+                assert np.array_equal(d.hit_voxel, want["hit_voxel"]), (trial, kind, T, skip)
+                assert np.array_equal(d.pixels, want["pixels"]), (trial, kind, T, skip)
+                hit = want["hit_voxel"][:, 0] >= 0
+                np.testing.assert_allclose(d.intensity[hit], want["intensity"][hit], atol=1e-12)
+
+
+def test_partitions_sum_to_full_frame(vx, small_sphere_volume, small_sphere_histogram):
+    from paper_1807_03119_b200.render import render_detail
+
+    cam = vx.orbit_camera(small_sphere_volume)
+    params = vx.RenderParams(width=61, height=45)
+    cfg = vx.FilterConfig(kind=vx.FilterKind.LOCAL_CLUSTER)
+    full = render_detail(small_sphere_volume, cam, params, cfg, small_sphere_histogram)
+    for world in (2, 3, 4, 8):
+        acc = np.zeros_like(full.pixels, dtype=np.int64)
+        owned = np.zeros_like(full.pixels, dtype=np.int64)
+        hits = 0
+        for r in range(world):
+            d = render_detail(small_sphere_volume, cam, params, cfg, small_sphere_histogram,
+                              partition=(r, world))
+            acc += d.pixels
+            hits += d.hit_count
+        assert np.array_equal(acc, full.pixels) and hits == full.hit_count, world
+
+
+# --- C2 / C3 (512^3 insect, 1024^2) against the frozen reference frames --------------------
+
+
+@pytest.mark.skipif(not (GOLDEN / "frames_c2.npz").exists(), reason="C2 fixture not frozen")
+def test_c2_c3_frames_match_reference(vx):
+    from paper_1807_03119_b200 import phantoms
+    from paper_1807_03119_b200.metrics import entropy_from_counts
+    from paper_1807_03119_b200.render import render_detail
+    from paper_1807_03119_b200.volume import generate_phantom_device
+
+    g = golden("frames_c2.npz")
+    spec = phantoms.insect_phantom_spec(512)
+    dev = generate_phantom_device(spec)
+    data = dev.read()
+    v = vx.Volume(dims=spec.dims, data=data)
+    object.__setattr__(v, "_vx_device", dev)
+    if v.content_hash() != str(g["sha256"]):
+        pytest.fail("device phantom differs from the reference phantom bytes")
+    h = vx.build_histogram(v)
+    assert np.array_equal(h.counts, g["counts"]) and h.otsu_threshold == int(g["otsu"])
+    cam = vx.orbit_camera(v)
+    params = vx.RenderParams(width=1024, height=1024)
+    for kind in KINDS:
+        d = render_detail(v, cam, params, cfg_for(vx, kind), h, diagnostics=True)
+        assert hashlib.sha256(d.hit_voxel.tobytes()).hexdigest() == str(g[f"{kind}__voxel_sha"]), kind
+        assert np.array_equal(d.pixels, g[f"{kind}__pixels"]), kind
+        assert d.hit_count == int(g[f"{kind}__hits"])
+        H = entropy_from_counts(d.image_hist, 1024 * 1024)
+        assert abs(H - float(g[f"{kind}__H"])) <= 1e-12
+        assert abs(vx.image_entropy(d.pixels) - float(g[f"{kind}__H"])) <= 1e-3

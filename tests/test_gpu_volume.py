@@ -1,0 +1,110 @@
+"""K3 volume ingestion (load_raw 8/16-bit, slice stacks), the device replica,
+the exact-skip distance map and the K7 phantom generator (mirrors
+tests/test_volume.py of the reference)."""
+
+from __future__ import annotations
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden
+
+pytestmark = pytest.mark.gpu
+
+
+def test_load_raw_8bit_roundtrip(vx, tmp_path):
+    rs = np.random.default_rng(1)
+    v = vx.Volume(dims=(7, 5, 3), data=rs.integers(0, 256, 105, dtype=np.uint8))
+    vx.save_raw(v, tmp_path / "a.raw")
+    w = vx.load_raw(tmp_path / "a.raw")
+    assert w.dims == (7, 5, 3) and np.array_equal(w.data, v.data)
+    from paper_1807_03119_b200.volume import device_volume
+
+    assert np.array_equal(device_volume(w).read(), v.data)
+
+
+def test_load_raw_16bit_rescale_exhaustive(vx, tmp_path):
+    g = golden("shading.npz")
+    wide = np.arange(65536, dtype="<u2")
+    (tmp_path / "w.raw").write_bytes(wide.tobytes())
+    meta = vx.VolumeMeta(dims=(256, 256, 1), bit_depth=16)
+    v = vx.load_raw(tmp_path / "w.raw", meta)
+    assert np.array_equal(v.data.reshape(-1), g["u16_rescale"])
+    # histogram of the rescaled volume is the device one
+    assert np.array_equal(vx.build_histogram(v).counts, np.bincount(g["u16_rescale"], minlength=256))
+
+
+def test_load_raw_errors(vx, tmp_path):
+    from paper_1807_03119_b200.volume import VolumeError
+
+    (tmp_path / "b.raw").write_bytes(b"\0" * 10)
+    with pytest.raises(VolumeError, match="expected 8 bytes.*file has 10"):
+        vx.load_raw(tmp_path / "b.raw", vx.VolumeMeta(dims=(2, 2, 2)))
+    with pytest.raises(FileNotFoundError):
+        vx.load_raw(tmp_path / "nope.raw")
+    with pytest.raises(VolumeError):
+        vx.load_raw(tmp_path / "b.raw")
+
+
+def test_slice_stack(vx, tmp_path):
+    from paper_1807_03119_b200.images import write_pgm
+
+    rs = np.random.default_rng(2)
+    slices = rs.integers(0, 256, (4, 6, 5), dtype=np.uint8)
+    for i, s in enumerate(slices):
+        write_pgm(s, tmp_path / f"s{i:02d}.pgm")
+    v = vx.load_slice_stack(tmp_path)
+    assert v.dims == (5, 6, 4) and np.array_equal(v.data, slices)
+
+
+@pytest.mark.parametrize("name", ["spot_64", "latency_64", "latency_128", "bench_128"])
+def test_device_phantom_matches_reference_bytes(vx, name):
+    meta = json.loads((GOLDEN / "phantoms.json").read_text())[name]
+    spec = vx.PhantomSpec.from_json(meta["spec"])
+    v = vx.generate_phantom(spec)
+    assert v.content_hash() == meta["sha256"]
+
+
+def test_device_phantom_vs_oracle_generator_256(vx, oracle):
+    from paper_1807_03119_b200 import phantoms
+
+    spec = phantoms.insect_phantom_spec(256)
+    v = vx.generate_phantom(spec)
+    ref = oracle.phantom(spec.to_json(), threads=oracle.max_threads())
+    assert int((v.data != ref).sum()) == 0
+
+
+def _brute_distance(bmax_occ: np.ndarray, cap: int) -> np.ndarray:
+    occ = np.argwhere(bmax_occ)
+    mz, my, mx = bmax_occ.shape
+    out = np.full(bmax_occ.shape, cap, dtype=np.int64)
+    if len(occ) == 0:
+        return out
+    zz, yy, xx = np.meshgrid(np.arange(mz), np.arange(my), np.arange(mx), indexing="ij")
+    for oz, oy, ox in occ:
+        d = np.maximum(np.maximum(abs(zz - oz), abs(yy - oy)), abs(xx - ox))
+        out = np.minimum(out, d)
+    return out
+
+
+def test_distance_map_is_exact_chebyshev(vx):
+    from paper_1807_03119_b200.volume import device_volume
+
+    rs = np.random.default_rng(4)
+    data = rs.integers(0, 50, (70, 41, 33), dtype=np.uint8)
+    for _ in range(12):
+        z, y, x = rs.integers(0, 70), rs.integers(0, 41), rs.integers(0, 33)
+        data[z, y, x] = 200
+    v = vx.Volume(dims=(33, 41, 70), data=data)
+    dv = device_volume(v)
+    dm = dv.distance_map(100).astype(np.int64)
+    nbz, nby, nbx = (70 + 7) // 8, (41 + 7) // 8, (33 + 7) // 8
+    pad = np.zeros((nbz * 8, nby * 8, nbx * 8), dtype=np.uint8)
+    pad[:70, :41, :33] = data
+    bmax = pad.reshape(nbz, 8, nby, 8, nbx, 8).max(axis=(1, 3, 5))
+    occ = np.zeros((nbz + 2, nby + 2, nbx + 2), dtype=bool)
+    occ[1:-1, 1:-1, 1:-1] = bmax >= 100
+    want = _brute_distance(occ, 24)
+    assert np.array_equal(dm, want)

@@ -1,0 +1,188 @@
+"""Host-side logic of the drop-in (CPU only): validation errors and messages,
+JSON round trips, offset tables, phantom specs, the native struct packing."""
+
+from __future__ import annotations
+
+import json
+import math
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden
+
+
+def test_filter_config_validation(vx):
+    from paper_1807_03119_b200.filters import FilterError
+
+    with pytest.raises(FilterError):
+        vx.FilterConfig(kernel_size=4)
+    with pytest.raises(FilterError):
+        vx.FilterConfig(kernel_size=1)
+    with pytest.raises(FilterError):
+        vx.FilterConfig(threshold=-1)
+    with pytest.raises(FilterError):
+        vx.FilterConfig(okada_threshold=-0.5)
+    with pytest.raises(FilterError):
+        vx.FilterConfig(cluster_offset=0)
+    with pytest.raises(FilterError, match="none, mean, sigma, okada, entropy, local-cluster"):
+        vx.FilterKind.from_name("nosuch")
+
+
+def test_filter_config_json_digest(vx):
+    cfg = vx.FilterConfig(kind=vx.FilterKind.OKADA, kernel_size=5, threshold=101.0,
+                          okada_threshold=30.0)
+    assert vx.FilterConfig.from_json(cfg.to_json()) == cfg
+    a = vx.FilterConfig(kind=vx.FilterKind.MEAN)
+    b = vx.FilterConfig(kind=vx.FilterKind.MEAN, threshold=100.0)
+    assert a.digest() != b.digest() and len(a.digest()) == 8
+
+
+def test_resolve_threshold(vx):
+    from paper_1807_03119_b200.filters import FilterError
+
+    class H:
+        otsu_threshold = 46
+
+    assert vx.FilterConfig().resolve_threshold(H()).threshold == 46.0
+    assert vx.FilterConfig(threshold=5.0).resolve_threshold(H()).threshold == 5.0
+    with pytest.raises(FilterError, match="histogram"):
+        vx.FilterConfig().resolve_threshold(None)
+
+
+def test_offset_tables_match_reference_definitions():
+    from paper_1807_03119_b200.filters import axis_arm_offsets, cluster_offsets, kernel_offsets
+
+    k = kernel_offsets(3)
+    assert k.shape == (27, 3) and tuple(k[0]) == (-1, -1, -1) and tuple(k[1]) == (-1, -1, 0)
+    assert axis_arm_offsets(3).shape == (9, 3)
+    c = cluster_offsets(3, 1)
+    assert c.shape == (81, 3)
+    assert np.abs(c).max() == 2
+    assert kernel_offsets(5).shape == (125, 3)
+
+
+def test_camera_and_params_validation(vx):
+    from paper_1807_03119_b200.render import RenderError
+
+    with pytest.raises(RenderError):
+        vx.Camera(position=(0, 0, 10), look_at=(0, 0, 0), up=(0, 0, 1))
+    with pytest.raises(RenderError):
+        vx.Camera(position=(1, 0, 0), look_at=(0, 0, 0), fov_y_deg=0)
+    with pytest.raises(RenderError):
+        vx.Camera(position=(1, 0, 0), look_at=(0, 0, 0), fov_y_deg=180)
+    with pytest.raises(RenderError):
+        vx.RenderParams(width=0)
+    with pytest.raises(RenderError):
+        vx.RenderParams(step_size=0)
+    with pytest.raises(RenderError):
+        vx.RenderParams(background=256)
+    cam = vx.Camera(position=(10, 4, 7), look_at=(0, 0, 0))
+    r, u, f = cam.basis()
+    for v in (r, u, f):
+        assert np.linalg.norm(v) == pytest.approx(1.0)
+    assert vx.Camera.from_json(cam.to_json()) == cam
+    p = vx.RenderParams(width=17, light_direction=(0.0, 1.0, 0.0))
+    assert vx.RenderParams.from_json(p.to_json()) == p
+
+
+def test_chunk_rule():
+    from paper_1807_03119_b200.render import chunk_for
+
+    assert chunk_for(0.5) == (16, False)
+    assert chunk_for(1.0) == (15, False)
+    assert chunk_for(2.5) == (6, False)
+    assert chunk_for(16.0) == (1, True)
+    assert chunk_for(15.0) == (1, False)
+    assert chunk_for(14.0) == (1, False)
+
+
+def test_orbit_camera_matches_oracle(vx, oracle):
+    v = vx.Volume(dims=(64, 32, 16), data=np.zeros(64 * 32 * 16, np.uint8))
+    cam = vx.orbit_camera(v, azimuth_deg=30, elevation_deg=95)
+    pos, look = oracle.orbit((64, 32, 16), 30, 95)
+    assert cam.position == pos and cam.look_at == look
+
+
+def test_volume_validation(vx):
+    from paper_1807_03119_b200.volume import VolumeError
+
+    with pytest.raises(VolumeError):
+        vx.Volume(dims=(2, 2, 2), data=np.zeros(7, np.uint8))
+    with pytest.raises(VolumeError):
+        vx.Volume(dims=(0, 2, 2), data=np.zeros(0, np.uint8))
+    v = vx.Volume(dims=(3, 2, 1), data=np.arange(6, dtype=np.uint8))
+    assert v.sample(2, 1, 0) == 5 and v.sample(3, 0, 0) == 0 and v.sample(-1, 0, 0) == 0
+    assert not v.data.flags.writeable
+
+
+def test_content_hash_matches_reference_definition(vx):
+    meta = json.loads((GOLDEN / "phantoms.json").read_text())["spot_64"]
+    from oracle.rng_np import generate_phantom_np
+
+    spec = vx.PhantomSpec.from_json(meta["spec"])
+    v = vx.Volume(dims=spec.dims, data=generate_phantom_np(spec.to_json()))
+    assert v.content_hash() == meta["sha256"]
+
+
+def test_phantom_specs_match_reference(vx):
+    from paper_1807_03119_b200 import phantoms
+
+    meta = json.loads((GOLDEN / "phantoms.json").read_text())
+    assert phantoms.spot_phantom_spec(64).to_json() == meta["spot_64"]["spec"]
+    assert phantoms.speckle_phantom_spec(128).to_json() == meta["speckle_128"]["spec"]
+    assert phantoms.latency_phantom_spec(128).to_json() == meta["latency_128"]["spec"]
+    assert phantoms.bench_phantom_spec(128).to_json() == meta["bench_128"]["spec"]
+
+
+@pytest.mark.skipif(not (GOLDEN / "frames_c2.npz").exists(), reason="C2 fixture not frozen")
+def test_insect_spec_is_the_survey_c2_recipe():
+    from paper_1807_03119_b200 import phantoms
+
+    g = golden("frames_c2.npz")
+    ref = json.loads(str(g["spec_json"]))
+    mine = phantoms.insect_phantom_spec(512).to_json()
+    assert mine == ref
+
+
+def test_rng_matches_oracle():
+    from oracle import rng_np
+    from paper_1807_03119_b200 import rng
+
+    assert rng.substream_seed(20, 0x73706F74) == rng_np.substream_seed(20, 0x73706F74)
+    assert np.array_equal(rng.stream(5, 3, 100), rng_np.stream(5, 3, 100))
+    a = rng.uniform_indices(123, 500, 1000)
+    assert len(set(a.tolist())) == 500 and a.max() < 1000
+    assert np.array_equal(a, rng_np.uniform_indices(123, 500, 1000))
+
+
+def test_native_config_packing(vx):
+    from paper_1807_03119_b200.filters import native_config
+
+    counts = np.zeros(256, dtype=np.int64)
+    counts[[0, 10, 200]] = [5, 3, 2]
+
+    class H:
+        probabilities = counts / counts.sum()
+        global_sigma = 12.5
+
+    cfg = vx.FilterConfig(kind=vx.FilterKind.SIGMA, threshold=67.0, sigma_mult=2.0)
+    fc = native_config(cfg, H())
+    assert fc.kind == 2 and fc.threshold == 67.0 and fc.sigma_band == 25.0
+    lut = np.ctypeslib.as_array(fc.entropy_lut)
+    p = 0.5
+    assert lut[0] == -p * math.log2(p)
+    assert lut[1] == 0.0
+
+
+def test_histogram_validation_messages():
+    from paper_1807_03119_b200.histogram import HistogramError, _as_u64_counts
+
+    with pytest.raises(HistogramError, match="expected 256 bins"):
+        _as_u64_counts([1, 2, 3])
+    with pytest.raises(HistogramError, match="non-negative"):
+        _as_u64_counts([-1] + [0] * 255)
+    with pytest.raises(HistogramError, match="empty"):
+        _as_u64_counts([0] * 256)
+    with pytest.raises(HistogramError, match="exact"):
+        _as_u64_counts([2 ** 47] + [0] * 255)
