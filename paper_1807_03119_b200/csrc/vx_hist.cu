@@ -235,26 +235,36 @@ __global__ void __launch_bounds__(256) otsu_kernel(const unsigned long long* __r
 // K6 finalisation: H = -sum(p * log2 p) over non-empty bins, p = c / n, in
 // numpy's pairwise summation order (numpy/_core/src/umath/loops_utils.h
 // pairwise_sum: <8 sequential from 0, <=128 eight accumulators, else split).
-__device__ double pairwise(const double* a, int n) {
+__device__ double pw_block(const double* a, int n) {
   if (n < 8) {
     double r = 0.0;
     for (int i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
     return r;
   }
-  if (n <= 128) {
-    double r[8];
-    for (int j = 0; j < 8; ++j) r[j] = a[j];
-    int i = 8;
-    for (; i < n - (n % 8); i += 8)
-      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
-    return res;
-  }
+  double r[8];
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+  return res;
+}
+
+__device__ double pw_level(const double* a, int n) {  // n <= 256
+  if (n <= 128) return pw_block(a, n);
   int n2 = n / 2;
   n2 -= n2 % 8;
-  return __dadd_rn(pairwise(a, n2), pairwise(a + n2, n - n2));
+  return __dadd_rn(pw_block(a, n2), pw_block(a + n2, n - n2));
+}
+
+// n <= 256 (non-empty bins): at most two split levels
+__device__ double pairwise(const double* a, int n) {
+  if (n <= 128) return pw_block(a, n);
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pw_level(a, n2), pw_level(a + n2, n - n2));
 }
 
 __global__ void entropy_kernel(const unsigned long long* __restrict__ counts, uint64_t n,

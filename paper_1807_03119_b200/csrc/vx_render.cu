@@ -106,7 +106,45 @@ __device__ __forceinline__ int rd(const VolView& V, long long x, long long y, lo
 // ---------------------------------------------------------------------------
 // filters (filters.py:165-227); integer sums, FP64 quotient
 
-__device__ double pairwise_sum(const double* a, int n);
+// numpy pairwise_sum (numpy/_core/src/umath/loops_utils.h) over a virtual
+// array a(k): n < 8 sequential from 0; n <= 128 eight accumulators; larger n
+// splits at n2 = n/2 - (n/2)%8.  Non-recursive (n <= 512: two split levels)
+// so the kernels keep a static stack.
+template <typename F>
+__device__ double pw_block(const F& a, int off, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, a(off + i));
+    return r;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = a(off + j);
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a(off + i + j));
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, a(off + i));
+  return res;
+}
+
+template <typename F>
+__device__ double pw_level(const F& a, int off, int n) {  // n <= 256
+  if (n <= 128) return pw_block(a, off, n);
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pw_block(a, off, n2), pw_block(a, off + n2, n - n2));
+}
+
+template <typename F>
+__device__ double pairwise_sum(const F& a, int n) {  // n <= 512
+  if (n <= 128) return pw_block(a, 0, n);
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pw_level(a, 0, n2), pw_level(a, n2, n - n2));
+}
 
 template <bool CHECKED>
 __device__ double filter_lc(const VolView& V, const FiltD& F, long long x, long long y,
@@ -197,12 +235,12 @@ __device__ double filter_entropy(const VolView& V, const FiltD& F, const double*
   if (PAIRWISE) {
     // a single-coordinate batch: numpy sums the contiguous (M^3, 1) column
     // with pairwise_sum (SURVEY.md Appendix B exp. 7)
-    double terms[343];  // M <= 7 (checked by the host)
-    int k = 0;
-    for (int dx = -h; dx <= h; ++dx)
-      for (int dy = -h; dy <= h; ++dy)
-        for (int dz = -h; dz <= h; ++dz) terms[k++] = lut[rd<CHECKED>(V, x + dx, y + dy, z + dz)];
-    H = pairwise_sum(terms, k);
+    const int M = F.M;
+    auto term = [&](int k) {
+      const int dz = k % M - h, dy = (k / M) % M - h, dx = k / (M * M) - h;
+      return lut[rd<CHECKED>(V, x + dx, y + dy, z + dz)];
+    };
+    H = pairwise_sum(term, M * M * M);  // M <= 7 (checked by the host)
   } else {
     // >= 2 coordinates: row-by-row (sequential) reduction over axis 0
     bool first = true;
@@ -241,29 +279,6 @@ __device__ __forceinline__ double filter_value(const VolView& V, const FiltD& F,
   if (KIND == VX_FILTER_ENTROPY) return filter_entropy<CHECKED, PAIRWISE>(V, F, lut, x, y, z);
   if (KIND == kAxisCluster) return filter_axis<CHECKED>(V, F, x, y, z);
   return filter_lc<CHECKED>(V, F, x, y, z);
-}
-
-// numpy pairwise_sum (loops_utils.h) for the single-coordinate entropy batch
-__device__ double pairwise_sum(const double* a, int n) {
-  if (n < 8) {
-    double r = 0.0;
-    for (int i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
-    return r;
-  }
-  if (n <= 128) {
-    double r[8];
-    for (int j = 0; j < 8; ++j) r[j] = a[j];
-    int i = 8;
-    for (; i < n - (n % 8); i += 8)
-      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
-    return res;
-  }
-  int n2 = n / 2;
-  n2 -= n2 % 8;
-  return __dadd_rn(pairwise_sum(a, n2), pairwise_sum(a + n2, n - n2));
 }
 
 // ---------------------------------------------------------------------------

@@ -29,7 +29,7 @@ __global__ void brick_max_kernel(const uint8_t* __restrict__ origin, int64_t sy,
 #pragma unroll
     for (int y = 0; y < 8; ++y) {
       const uint2 w = __ldg(reinterpret_cast<const uint2*>(p0 + z * sz + y * sy));
-      m = max(m, __vmaxu4(w.x, w.y));
+      m = __vmaxu4(m, __vmaxu4(w.x, w.y));
     }
   }
   m = max(max(m & 0xffu, (m >> 8) & 0xffu), max((m >> 16) & 0xffu, m >> 24));
