@@ -239,7 +239,10 @@ def run_ours(args):
     fc = native_config(cfg, hist)
     part = _lib.vx_partition(rank, world)
 
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-null) stream: the C-ABI treats stream 0 as "the calling
+    # thread's own stream", so torch work, events and our kernels share this one
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     sptr = C.c_void_p(stream.cuda_stream)
     pixels = torch.zeros(H * W, dtype=torch.uint8, device="cuda")
     small = torch.zeros(260, dtype=torch.int64, device="cuda")
@@ -329,7 +332,10 @@ def run_ours(args):
             torch.cuda.synchronize()
             if i >= 3:
                 hk.append(a.elapsed_time(b))
-        assert np.array_equal(dcounts.cpu().numpy(), counts) and int(dT.item()) == hist.otsu_threshold
+        got = dcounts.cpu().numpy()
+        if not (np.array_equal(got, counts) and int(dT.item()) == hist.otsu_threshold):
+            raise SystemExit(f"K1/K2 mismatch: T {int(dT.item())} vs {hist.otsu_threshold}, "
+                             f"{int((got != counts).sum())} bins differ")
         hms = statistics.median(hk)
         peak, peak_kind = peaks()
         gbs = nvox / (hms * 1e-3) / 1e9
