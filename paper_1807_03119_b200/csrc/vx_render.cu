@@ -151,7 +151,7 @@ __device__ double filter_lc(const VolView& V, const FiltD& F, long long x, long 
                             long long z) {
   long long sum = 0;
   const int h = (F.M - 1) >> 1;
-#pragma unroll 1
+#pragma unroll 3
   for (int c = 0; c < 9; ++c) {
     long long cx = x, cy = y, cz = z;
     if (c > 0) {
@@ -393,23 +393,45 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
         if (skipped) continue;
       }
     }
-    // exact samples of this chunk (render.py:295-329)
+    // exact samples of this chunk (render.py:295-329).
     uint32_t cand = 0;
-#pragma unroll 4
-    for (int k = 0; k < m; ++k) {
-      const float tk = __fadd_rn(base, M.sk[k]);
-      if (!(tk <= tend)) break;  // t_k is monotone in k
-      float px = pos1(R.o[0], tk, R.d[0]);
-      float py = pos1(R.o[1], tk, R.d[1]);
-      float pz = pos1(R.o[2], tk, R.d[2]);
-      if (M.need_clip) {
-        px = clip1(px, M.xmax);
-        py = clip1(py, M.ymax);
-        pz = clip1(pz, M.zmax);
+    if (m == 16 && !M.need_clip) {
+      // Full 16-sample chunk: every voxel load is issued before any is
+      // consumed (16-deep MLP per ray).  Samples past the exit lie at most
+      // 15*step < 15 voxels outside the box, inside the zero apron
+      // (VX_PAD = 16) -- the reference's own argument for unclamped overshoot
+      // reads (render.py:283-285, 300-305); tk <= tend masks them below.
+      int raw[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const float tk = __fadd_rn(base, M.sk[k]);
+        raw[k] = rd<false>(V, __float2int_rz(pos1(R.o[0], tk, R.d[0])),
+                           __float2int_rz(pos1(R.o[1], tk, R.d[1])),
+                           __float2int_rz(pos1(R.o[2], tk, R.d[2])));
       }
-      const int raw = rd<false>(V, __float2int_rz(px), __float2int_rz(py), __float2int_rz(pz));
-      ++nsamp;
-      if (raw >= M.thr) cand |= 1u << k;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        if (__fadd_rn(base, M.sk[k]) <= tend) {
+          ++nsamp;
+          if (raw[k] >= M.thr) cand |= 1u << k;
+        }
+      }
+    } else {
+      for (int k = 0; k < m; ++k) {
+        const float tk = __fadd_rn(base, M.sk[k]);
+        if (!(tk <= tend)) break;  // t_k is monotone in k
+        float px = pos1(R.o[0], tk, R.d[0]);
+        float py = pos1(R.o[1], tk, R.d[1]);
+        float pz = pos1(R.o[2], tk, R.d[2]);
+        if (M.need_clip) {
+          px = clip1(px, M.xmax);
+          py = clip1(py, M.ymax);
+          pz = clip1(pz, M.zmax);
+        }
+        const int raw = rd<false>(V, __float2int_rz(px), __float2int_rz(py), __float2int_rz(pz));
+        ++nsamp;
+        if (raw >= M.thr) cand |= 1u << k;
+      }
     }
     while (cand) {
       const int k = __ffs(cand) - 1;
@@ -507,13 +529,11 @@ __device__ __forceinline__ int own_budget(double te, double tx, double step) {
 template <int KIND, bool CHECKED>
 __global__ void __launch_bounds__(kTileW * kTileH) raycast_kernel(const RenderArgs a) {
   __shared__ double lut[KIND == VX_FILTER_ENTROPY ? 256 : 1];
-  __shared__ unsigned int hist[256];
   const int tid = threadIdx.y * kTileW + threadIdx.x;
-  if (KIND == VX_FILTER_ENTROPY)
+  if (KIND == VX_FILTER_ENTROPY) {
     for (int i = tid; i < 256; i += kTileW * kTileH) lut[i] = a.lut[i];
-  if (a.O.image_hist)
-    for (int i = tid; i < 256; i += kTileW * kTileH) hist[i] = 0u;
-  __syncthreads();
+    __syncthreads();
+  }
 
   const int tile = a.rank + a.world * (int)blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
@@ -523,6 +543,7 @@ __global__ void __launch_bounds__(kTileW * kTileH) raycast_kernel(const RenderAr
 
   bool hit = false;
   unsigned nsamp = 0;
+  uint8_t pix_out = 0;
   if (valid) {
     double d[3];
     ray_dir(a.C, i, j, d);
@@ -568,18 +589,22 @@ __global__ void __launch_bounds__(kTileW * kTileH) raycast_kernel(const RenderAr
     if (a.O.hit_t) a.O.hit_t[p] = hit ? ht : 0.0f;
     if (a.O.hit_value) a.O.hit_value[p] = hit ? hval : 0.0;
     if (a.O.intensity) a.O.intensity[p] = I;
-    if (a.O.image_hist) atomicAdd(&hist[pix], 1u);
+    pix_out = pix;
   }
-  const int nhit = __syncthreads_count(hit);
-  if (tid == 0 && a.O.hit_count && nhit) atomicAdd(a.O.hit_count, (unsigned long long)nhit);
+  // warp-level aggregation (no block barrier: warps retire independently)
+  const unsigned lane = tid & 31u;
+  const unsigned hits = __ballot_sync(0xffffffffu, hit);
+  if (lane == 0 && a.O.hit_count && hits) atomicAdd(a.O.hit_count, (unsigned long long)__popc(hits));
   if (a.O.samples) {
     unsigned s = nsamp;
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((tid & 31) == 0 && s) atomicAdd(a.O.samples, (unsigned long long)s);
+    if (lane == 0 && s) atomicAdd(a.O.samples, (unsigned long long)s);
   }
   if (a.O.image_hist) {
-    for (int b = tid; b < 256; b += kTileW * kTileH)
-      if (hist[b]) atomicAdd(a.O.image_hist + b, (unsigned long long)hist[b]);
+    const unsigned key = valid ? (unsigned)pix_out : 0x100u;
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    if (valid && (__ffs(peers) - 1) == (int)lane)
+      atomicAdd(a.O.image_hist + pix_out, (unsigned long long)__popc(peers));
   }
 }
 
