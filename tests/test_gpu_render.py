@@ -265,3 +265,49 @@ def test_c2_c3_frames_match_reference(vx):
         H = entropy_from_counts(d.image_hist, 1024 * 1024)
         assert abs(H - float(g[f"{kind}__H"])) <= 1e-12
         assert abs(vx.image_entropy(d.pixels) - float(g[f"{kind}__H"])) <= 1e-3
+
+
+def test_partition_matches_owned_mask(vx, small_sphere_volume, small_sphere_histogram):
+    from paper_1807_03119_b200.distributed import owned_pixel_mask
+    from paper_1807_03119_b200.render import render_detail
+
+    cam = vx.orbit_camera(small_sphere_volume)
+    params = vx.RenderParams(width=70, height=50, background=7)
+    cfg = vx.FilterConfig(kind=vx.FilterKind.MEAN)
+    full = render_detail(small_sphere_volume, cam, params, cfg, small_sphere_histogram).pixels
+    for world in (2, 3):
+        for r in range(world):
+            d = render_detail(small_sphere_volume, cam, params, cfg, small_sphere_histogram,
+                              partition=(r, world))
+            m = owned_pixel_mask(70, 50, r, world)
+            assert np.array_equal(d.pixels, np.where(m, full, 0))
+
+
+def test_sharded_api_single_rank_nccl(vx, small_sphere_volume, small_sphere_histogram):
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1807_03119_b200.distributed import histogram_sharded, render_sharded
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        h = histogram_sharded(small_sphere_volume.data)
+        assert np.array_equal(h.counts, small_sphere_histogram.counts)
+        assert h.otsu_threshold == small_sphere_histogram.otsu_threshold
+        cam = vx.orbit_camera(small_sphere_volume)
+        params = vx.RenderParams(width=64, height=40)
+        cfg = vx.FilterConfig(kind=vx.FilterKind.LOCAL_CLUSTER)
+        f = render_sharded(small_sphere_volume, cam, params, cfg, h)
+        ref = vx.render_frame(small_sphere_volume, cam, params, cfg, h)
+        assert np.array_equal(f.pixels, ref.pixels) and f.hit_count == ref.hit_count
+        assert np.array_equal(f.image_hist, np.bincount(ref.pixels.reshape(-1), minlength=256))
+    finally:
+        dist.destroy_process_group()
