@@ -107,6 +107,10 @@ typedef struct {
   uint64_t* image_hist;  /* [256] grey-level histogram of pixels (fused K6) */
   uint64_t* hit_count;   /* [1]                                             */
   uint64_t* samples;     /* [1] march samples taken (diagnostic)            */
+  uint64_t* diag;        /* [8] march statistics (diagnostic, nullable):
+                            distance lookups, skips, chunks skipped, (unused),
+                            sample groups, filter evaluations, hits, ray
+                            iterations                                        */
   int32_t* trunc_flag;   /* [1] set to 1 when a ray exhausted its own
                             span-derived step budget max(1, ceil(span/step)+1)
                             without ending; only then can the frame-wide
@@ -208,9 +212,12 @@ int vx_phantom_device(uint8_t* dev_out, int64_t nx, int64_t ny, int64_t nz,
 /* ---- diagnostics ---------------------------------------------------------- */
 /* number of kernels this thread launched since the last reset */
 int vx_launch_counter(uint64_t* n_out, int reset);
-/* exact-skip structure for threshold thr: Chebyshev brick distance map
- * (dims (nbz+2)*(nby+2)*(nbx+2)) copied to host; for tests */
-int vx_volume_distance_map(vx_volume* vol, int32_t thr, uint8_t* host_out, int64_t dims_out[3]);
+/* exact-skip structures for threshold thr, copied to host (tests):
+ * level 0 = Chebyshev distance in 8^3 bricks to the nearest brick whose max
+ * reaches thr (dims ceil(n/8)+2 per axis, 1-brick apron, capped at 24);
+ * level 1 = the same over 2^3 cells (dims ceil(n/2)+2, capped at 8). */
+int vx_volume_distance_map(vx_volume* vol, int32_t thr, int32_t level, uint8_t* host_out,
+                           int64_t dims_out[3]);
 
 #ifdef __cplusplus
 }

@@ -95,6 +95,7 @@ class vx_render_out(C.Structure):
         ("image_hist", C.c_void_p),
         ("hit_count", C.c_void_p),
         ("samples", C.c_void_p),
+        ("diag", C.c_void_p),
         ("trunc_flag", C.c_void_p),
     ]
 
@@ -134,7 +135,7 @@ SIGNATURES = {
     "vx_volume_create_phantom": [I64, I64, I64, P, I64, F64, U64, P, I64, I32, P],
     "vx_phantom_device": [P, I64, I64, I64, P, I64, F64, U64, P, I64, I32, P],
     "vx_launch_counter": [P, C.c_int],
-    "vx_volume_distance_map": [P, I32, P, P],
+    "vx_volume_distance_map": [P, I32, I32, P, P],
 }
 _RESTYPES = {"vx_last_error": C.c_char_p}
 

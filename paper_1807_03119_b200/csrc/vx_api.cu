@@ -109,6 +109,9 @@ VolView vx_view(const vx_volume* v, const uint8_t* dist_map) {
   V.bsy = v->bsy;
   V.bsz = v->bsz;
   V.dist = dist_map ? dist_map + v->bsz + v->bsy + 1 : nullptr;
+  V.csy = v->csy;
+  V.csz = v->csz;
+  V.dist2 = dist_map ? dist_map + v->map_bytes + v->csz + v->csy + 1 : nullptr;
   return V;
 }
 
@@ -143,6 +146,12 @@ int vx_volume_alloc(int64_t nx, int64_t ny, int64_t nz, vx_volume** out) {
   v->bsy = v->nbx + 2;
   v->bsz = (int64_t)(v->nbx + 2) * (v->nby + 2);
   v->map_bytes = (uint64_t)v->bsz * (v->nbz + 2);
+  v->ncx = (int)((nx + VX_CELL - 1) / VX_CELL);
+  v->ncy = (int)((ny + VX_CELL - 1) / VX_CELL);
+  v->ncz = (int)((nz + VX_CELL - 1) / VX_CELL);
+  v->csy = v->ncx + 2;
+  v->csz = (int64_t)(v->ncx + 2) * (v->ncy + 2);
+  v->cmap_bytes = (uint64_t)v->csz * (v->ncz + 2);
   for (auto& d : v->dist) {
     d.thr = -1;
     d.map = nullptr;
@@ -153,12 +162,13 @@ int vx_volume_alloc(int64_t nx, int64_t ny, int64_t nz, vx_volume** out) {
     delete v;
     return vx_cuda_fail(e, "cudaMalloc(volume)", __FILE__, __LINE__);
   }
-  e = cudaMalloc(&v->bmax, v->map_bytes);
+  e = cudaMalloc(&v->bmax, v->map_bytes + v->cmap_bytes);
   if (e != cudaSuccess) {
     cudaFree(v->alloc);
     delete v;
     return vx_cuda_fail(e, "cudaMalloc(brick map)", __FILE__, __LINE__);
   }
+  v->cmax = v->bmax + v->map_bytes;
   v->origin = v->alloc + VX_PAD * v->sz + VX_PAD * v->sy + VX_PAD;
   *out = v;
   return VX_OK;
@@ -181,8 +191,10 @@ int vx_volume_finish(vx_volume* v, const uint8_t* compact_dev, cudaStream_t s) {
   p.extent = make_cudaExtent(v->nx, v->ny, v->nz);
   p.kind = cudaMemcpyDeviceToDevice;
   VX_CUDA(cudaMemcpy3DAsync(&p, s));
-  VX_CUDA(cudaMemsetAsync(v->bmax, 0, v->map_bytes, s));
+  VX_CUDA(cudaMemsetAsync(v->bmax, 0, v->map_bytes + v->cmap_bytes, s));
   rc = vx_launch_brick_max(v, s);
+  if (rc) return rc;
+  rc = vx_launch_cell_max(v, s);
   if (rc) return rc;
   VX_CUDA(cudaMemcpyAsync(v->counts, dcounts, 256 * 8, cudaMemcpyDeviceToHost, s));
   VX_CUDA(cudaFreeAsync(dcounts, s));
@@ -342,7 +354,7 @@ extern "C" int vx_volume_device_bytes(const vx_volume* v, uint64_t* bytes_out) {
     vx_set_error("vx_volume_device_bytes: null argument");
     return VX_EINVAL;
   }
-  *bytes_out = v->alloc_bytes + v->map_bytes;
+  *bytes_out = v->alloc_bytes + v->map_bytes + v->cmap_bytes;
   return VX_OK;
 }
 
@@ -386,7 +398,7 @@ int vx_get_dist_map(vx_volume* v, int thr, const uint8_t** map_out, cudaStream_t
     // another thread's stream may still read the evicted map
     VX_CUDA(cudaDeviceSynchronize());
   } else {
-    VX_CUDA(cudaMalloc(&victim->map, v->map_bytes));
+    VX_CUDA(cudaMalloc(&victim->map, v->map_bytes + v->cmap_bytes));
   }
   victim->thr = -1;
   int rc = vx_launch_dist_map(v, thr, victim->map, s);
@@ -399,23 +411,24 @@ int vx_get_dist_map(vx_volume* v, int thr, const uint8_t** map_out, cudaStream_t
   return VX_OK;
 }
 
-extern "C" int vx_volume_distance_map(vx_volume* v, int32_t thr, uint8_t* host_out,
-                                      int64_t dims_out[3]) {
-  if (!v) {
-    vx_set_error("vx_volume_distance_map: null argument");
+extern "C" int vx_volume_distance_map(vx_volume* v, int32_t thr, int32_t level,
+                                      uint8_t* host_out, int64_t dims_out[3]) {
+  if (!v || (level != 0 && level != 1)) {
+    vx_set_error("vx_volume_distance_map: bad argument");
     return VX_EINVAL;
   }
   if (dims_out) {
-    dims_out[0] = v->nbx + 2;
-    dims_out[1] = v->nby + 2;
-    dims_out[2] = v->nbz + 2;
+    dims_out[0] = level ? v->ncx + 2 : v->nbx + 2;
+    dims_out[1] = level ? v->ncy + 2 : v->nby + 2;
+    dims_out[2] = level ? v->ncz + 2 : v->nbz + 2;
   }
   if (!host_out) return VX_OK;
   cudaStream_t s = vx_stream();
   const uint8_t* map = nullptr;
   int rc = vx_get_dist_map(v, thr, &map, s);
   if (rc) return rc;
-  VX_CUDA(cudaMemcpyAsync(host_out, map, v->map_bytes, cudaMemcpyDeviceToHost, s));
+  VX_CUDA(cudaMemcpyAsync(host_out, level ? map + v->map_bytes : map,
+                          level ? v->cmap_bytes : v->map_bytes, cudaMemcpyDeviceToHost, s));
   VX_CUDA(cudaStreamSynchronize(s));
   return VX_OK;
 }

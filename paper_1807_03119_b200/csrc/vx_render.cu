@@ -40,6 +40,8 @@ struct RayCamD {
 
 struct MarchD {
   float s;        // f32(step)
+  float inv_s;    // 1/s (estimates only)
+  float sk_last;  // fl(s * (chunk - 1))
   float adv;      // fl(f32(chunk) * s)
   float sk[16];   // fl(s * k), k < chunk
   float xmax, ymax, zmax;
@@ -75,6 +77,7 @@ struct OutD {
   unsigned long long* image_hist;
   unsigned long long* hit_count;
   unsigned long long* samples;
+  unsigned long long* diag;
   int32_t* trunc_flag;
 };
 
@@ -341,11 +344,21 @@ __device__ __forceinline__ void ray_span(const double o[3], const double d[3], i
 // the exact FP32 march (render.py:236-339) with exact skipping
 
 struct RayState {
-  float o[3];  // f32(origin + 0.5)
-  float d[3];  // f32(dir)
+  float o[3];    // f32(origin + 0.5)
+  float d[3];    // f32(dir)
+  float inv[3];  // 1/d (skip estimates only; +-inf for +-0)
+  float bo[3];   // exit-face offset minus origin: (inv > 0 ? -1/8 : 4 + 1/8) - o
   float base;
   float tend;
 };
+
+__device__ __forceinline__ void ray_skip_consts(RayState& R) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    R.inv[c] = __frcp_rn(R.d[c]);
+    R.bo[c] = (R.inv[c] > 0.0f ? -0.125f : (float)VX_CELL + 0.125f) - R.o[c];
+  }
+}
 
 __device__ __forceinline__ float pos1(float o, float t, float d) {
   return __fadd_rn(o, __fmul_rn(t, d));
@@ -358,108 +371,224 @@ __device__ __forceinline__ float clip1(float p, float hi) {
 
 enum MarchStatus { kMiss = 0, kHit = 1, kExhausted = 2 };
 
-// march one ray; limit = sample budget.  Returns kHit on an accepted hit,
-// kMiss when the ray leaves its span, kExhausted when the budget ran out.
-template <int KIND, bool CHECKED>
+// march statistics (vx_render_out.diag); compiled in only when requested
+struct Diag {
+  unsigned c[8];
+};
+enum DiagIndex { dLookup, dInChunk, dChunkLoop, dUnused, dGroup, dFilter, dHit, dIter };
+#define VX_DIAG(i) \
+  do {             \
+    if (DIAG) ++dg.c[i]; \
+  } while (0)
+
+constexpr int kGroup = 8;  // samples loaded together in occupied regions
+
+// t of sample k of the chunk starting at base: fl(base + fl(s * k))
+__device__ __forceinline__ float sample_t(float base, float s, int k) {
+  return __fadd_rn(base, __fmul_rn(s, (float)k));
+}
+
+// first index in [lo, m] whose sample t exceeds lim (m if none); O(1):
+// estimate, then fix up against the exact sample t (monotone in k)
+__device__ __forceinline__ int first_beyond(float base, const MarchD& M, float lim, int lo, int m) {
+  const float q = __fmul_rn(__fsub_rn(lim, base), M.inv_s);
+  int kn = q < 0.0f ? 0 : (q >= (float)m ? m : (int)q);
+  if (kn < lo) kn = lo;
+  while (kn < m && sample_t(base, M.s, kn) <= lim) ++kn;
+  while (kn > lo && sample_t(base, M.s, kn - 1) > lim) --kn;
+  return kn;
+}
+
+// March (render.py:236-339), one ray per lane, as a warp-synchronous
+// state machine.  Per ray: (done, k, base) = samples before the current
+// chunk, next sample index in the chunk, exact FP32 chunk base.  Each
+// iteration every running lane takes ONE step:
+//   * chunk finished -> exact base recurrence (render.py:331);
+//   * otherwise look up the fine Chebyshev cell distance D of the current
+//     sample's cell.  D >= 1: the box of cells within D-1 is empty (all
+//     max < thr); every sample up to the ray's exit from that box (less
+//     margins) is stepped over -- whole chunks by the base recurrence,
+//     single samples within a chunk -- and never loaded;
+//   * D == 0 (the sample's cell holds a candidate-level voxel): the lane
+//     needs its next kGroup samples.  Those are loaded cooperatively by the
+//     whole warp (4 rays x 8 samples per pass, ray state by shuffles), so
+//     the loads run at full SIMT width however few lanes need them; each
+//     owner then resolves its candidates (raw >= thr) in order and runs the
+//     filter until one is accepted (render.py:311-329).
+// wl: this warp's 32-int shared scratch.  All 32 lanes must call.
+// limit = the lane's sample budget.  Returns kHit, kMiss (left the span or
+// inactive) or kExhausted (budget ran out while still inside the span).
+template <int KIND, bool CHECKED, bool DIAG>
 __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const double* lut,
-                      RayState& R, int limit, int& hx, int& hy, int& hz, float& ht,
-                      double& hval, int& hidx, unsigned& nsamp) {
+                     const RayState& R, bool active, int limit, int& hx, int& hy, int& hz,
+                     float& ht, double& hval, int& hidx, unsigned& nsamp, Diag& dg, int* wl) {
+  constexpr int kRunning = 3;
+  const unsigned lane = (threadIdx.y * blockDim.x + threadIdx.x) & 31u;
+  int status = active ? kRunning : kMiss;
   int done = 0;
+  int k = 0;
   float base = R.base;
   const float tend = R.tend;
-  while (done < limit) {
-    int m = limit - done;
-    if (m > M.chunk) m = M.chunk;
-    if (M.skip && m == M.chunk) {
-      const int vx = __float2int_rz(pos1(R.o[0], base, R.d[0]));
-      const int vy = __float2int_rz(pos1(R.o[1], base, R.d[1]));
-      const int vz = __float2int_rz(pos1(R.o[2], base, R.d[2]));
-      const int bx = vx >> VX_BRICK_SHIFT, by = vy >> VX_BRICK_SHIFT, bz = vz >> VX_BRICK_SHIFT;
-      int D = 0;
-      if (bx >= -1 && by >= -1 && bz >= -1 && bx <= ((V.nx + 7) >> 3) && by <= ((V.ny + 7) >> 3) &&
-          bz <= ((V.nz + 7) >> 3))
-        D = __ldg(V.dist + (bz * V.bsz + by * V.bsy + bx));
-      if (D >= 2) {
-        const float lim = __fadd_rd(base, (float)(VX_BRICK * (D - 1)) - 0.0625f);
-        const float last = M.sk[M.chunk - 1];
-        bool skipped = false;
-        while (__fadd_rn(base, last) <= lim) {
-          base = __fadd_rn(base, M.adv);
-          done += M.chunk;
-          skipped = true;
-          if (!(base <= tend)) return kMiss;
-          if (limit - done < M.chunk) break;  // keep budget tails exact
+  const int chunk = M.chunk;
+  while (__any_sync(0xffffffffu, status == kRunning)) {
+    bool need = false;
+    int m = 0;
+    if (status == kRunning) {
+      VX_DIAG(dIter);
+      m = limit - done;
+      if (m > chunk) m = chunk;
+      if (k >= m) {  // chunk finished: exact base recurrence (render.py:331)
+        base = __fadd_rn(base, __fmul_rn((float)m, M.s));
+        done += m;
+        k = 0;
+        if (!(base <= tend))
+          status = kMiss;
+        else if (done >= limit)
+          status = kExhausted;
+      } else {
+        const float tk = sample_t(base, M.s, k);
+        if (!(tk <= tend)) {
+          // later samples of this chunk are beyond the exit too and the
+          // next chunk's base >= t_k: the reference drops the ray
+          status = kMiss;
+        } else if (M.skip) {
+          const int vx = __float2int_rz(pos1(R.o[0], tk, R.d[0]));
+          const int vy = __float2int_rz(pos1(R.o[1], tk, R.d[1]));
+          const int vz = __float2int_rz(pos1(R.o[2], tk, R.d[2]));
+          const int cx = vx >> VX_CELL_SHIFT, cy = vy >> VX_CELL_SHIFT, cz = vz >> VX_CELL_SHIFT;
+          // in-span samples truncate into [0, n]: inside the map's 1-cell apron
+          VX_DIAG(dLookup);
+          const int D = __ldg(V.dist2 + (cz * (int)V.csz + cy * (int)V.csy + cx));
+          float lim = -1.0f;
+          if (D >= 1) {
+            // cells within Chebyshev distance D-1 of this one: the box
+            // [4(c-D+1), 4(c+D)) per axis in p = pos + 0.5 coordinates, shrunk
+            // by 1/8 voxel; the exact ray (o, d) stays inside it from t_k to
+            // its exit t_box, so each sample with t <= t_box (less a t margin)
+            // truncates into an empty cell (FP32 position error < 2^-7 voxel
+            // for |p|, |t| < 8192).  Exit face per axis: 4(c+D) - 1/8 when
+            // d > 0, 4(c-D+1) + 1/8 when d < 0 (R.bo folds the offsets).
+            const int cc[3] = {cx, cy, cz};
+            float tb = 3.0e38f;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+              const int face = VX_CELL * (R.inv[a] > 0.0f ? cc[a] + D : cc[a] - D);
+              tb = fminf(tb, __fmul_rn(__fadd_rn((float)face, R.bo[a]), R.inv[a]));  // NaN ignored
+            }
+            lim = __fsub_rd(tb, __fmaf_ru(fabsf(tb), 1.0f / 524288.0f, 0.0625f));
+          }
+          if (lim > tk) {
+            // step over every sample with t <= lim: the rest of this chunk,
+            // whole chunks by the exact base recurrence, then into the chunk
+            // holding the first sample beyond lim
+            VX_DIAG(dInChunk);
+            int lo = k + 1;  // samples before lo lie within lim
+            for (;;) {
+              k = first_beyond(base, M, lim, lo, m);
+              if (k < m) break;
+              base = __fadd_rn(base, __fmul_rn((float)m, M.s));
+              done += m;
+              if (!(base <= tend)) { status = kMiss; break; }
+              if (done >= limit) { status = kExhausted; break; }
+              while (done + chunk <= limit && __fadd_rn(base, M.sk_last) <= lim) {
+                VX_DIAG(dChunkLoop);
+                base = __fadd_rn(base, M.adv);
+                done += chunk;
+              }
+              // intermediate bases are <= this one: if it passed the exit the
+              // reference dropped the ray at the first one that did
+              if (!(base <= tend)) { status = kMiss; break; }
+              if (done >= limit) { status = kExhausted; break; }
+              m = limit - done;
+              if (m > chunk) m = chunk;
+              lo = 0;
+            }
+          } else {
+            need = true;
+          }
+        } else {
+          need = true;
         }
-        if (skipped) continue;
       }
     }
-    // exact samples of this chunk (render.py:295-329).
-    uint32_t cand = 0;
-    if (m == 16 && !M.need_clip) {
-      // Full 16-sample chunk: every voxel load is issued before any is
-      // consumed (16-deep MLP per ray).  Samples past the exit lie at most
-      // 15*step < 15 voxels outside the box, inside the zero apron
-      // (VX_PAD = 16) -- the reference's own argument for unclamped overshoot
-      // reads (render.py:283-285, 300-305); tk <= tend masks them below.
-      int raw[16];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const float tk = __fadd_rn(base, M.sk[k]);
-        raw[k] = rd<false>(V, __float2int_rz(pos1(R.o[0], tk, R.d[0])),
-                           __float2int_rz(pos1(R.o[1], tk, R.d[1])),
-                           __float2int_rz(pos1(R.o[2], tk, R.d[2])));
-      }
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        if (__fadd_rn(base, M.sk[k]) <= tend) {
-          ++nsamp;
-          if (raw[k] >= M.thr) cand |= 1u << k;
-        }
-      }
-    } else {
-      for (int k = 0; k < m; ++k) {
-        const float tk = __fadd_rn(base, M.sk[k]);
-        if (!(tk <= tend)) break;  // t_k is monotone in k
-        float px = pos1(R.o[0], tk, R.d[0]);
-        float py = pos1(R.o[1], tk, R.d[1]);
-        float pz = pos1(R.o[2], tk, R.d[2]);
+    // ---- cooperative loads of the next kGroup samples of every needy lane ----
+    const unsigned gm = __ballot_sync(0xffffffffu, need);
+    if (gm) {
+      const int nr = __popc(gm);
+      const int rank = __popc(gm & ((1u << lane) - 1u));
+      if (need) wl[rank] = (int)lane;
+      __syncwarp();
+      unsigned my_c = 0, my_v = 0;
+      for (int b = 0; b < nr; b += 4) {
+        const int q = b + (int)(lane >> 3);
+        const int j = (int)(lane & 7u);
+        const int src = wl[q < nr ? q : 0];  // spare slots repeat a real ray: loads stay legal
+        const float sb = __shfl_sync(0xffffffffu, base, src);
+        const int sk = __shfl_sync(0xffffffffu, k, src);
+        const int sm = __shfl_sync(0xffffffffu, m, src);
+        const float st = __shfl_sync(0xffffffffu, tend, src);
+        const float o0 = __shfl_sync(0xffffffffu, R.o[0], src);
+        const float o1 = __shfl_sync(0xffffffffu, R.o[1], src);
+        const float o2 = __shfl_sync(0xffffffffu, R.o[2], src);
+        const float d0 = __shfl_sync(0xffffffffu, R.d[0], src);
+        const float d1 = __shfl_sync(0xffffffffu, R.d[1], src);
+        const float d2 = __shfl_sync(0xffffffffu, R.d[2], src);
+        // clamped to the chunk: samples past the exit lie <= chunk*step <= 15
+        // voxels outside the box, inside the zero apron (VX_PAD = 16) -- the
+        // reference's own argument for unclamped overshoot reads
+        // (render.py:283-285, 300-305)
+        const int kk = min(sk + j, max(sm - 1, 0));
+        const float t = sample_t(sb, M.s, kk);
+        float px = pos1(o0, t, d0), py = pos1(o1, t, d1), pz = pos1(o2, t, d2);
         if (M.need_clip) {
           px = clip1(px, M.xmax);
           py = clip1(py, M.ymax);
           pz = clip1(pz, M.zmax);
         }
         const int raw = rd<false>(V, __float2int_rz(px), __float2int_rz(py), __float2int_rz(pz));
-        ++nsamp;
-        if (raw >= M.thr) cand |= 1u << k;
+        const bool inr = q < nr && sk + j < sm && t <= st;
+        const unsigned bc = __ballot_sync(0xffffffffu, inr && raw >= M.thr);
+        const unsigned bv = __ballot_sync(0xffffffffu, inr);
+        if (need && rank >= b && rank < b + 4) {
+          const int sh = (rank - b) * 8;
+          my_c = (bc >> sh) & 0xffu;
+          my_v = (bv >> sh) & 0xffu;
+        }
+      }
+      __syncwarp();
+      if (need) {
+        VX_DIAG(dGroup);
+        nsamp += __popc(my_v);
+        while (my_c) {
+          const int j = __ffs(my_c) - 1;
+          my_c &= my_c - 1;
+          const float t = sample_t(base, M.s, k + j);
+          float px = pos1(R.o[0], t, R.d[0]);
+          float py = pos1(R.o[1], t, R.d[1]);
+          float pz = pos1(R.o[2], t, R.d[2]);
+          if (M.need_clip) {
+            px = clip1(px, M.xmax);
+            py = clip1(py, M.ymax);
+            pz = clip1(pz, M.zmax);
+          }
+          const int cx = __float2int_rz(px), cy = __float2int_rz(py), cz = __float2int_rz(pz);
+          VX_DIAG(dFilter);
+          const double f = filter_value<KIND, CHECKED>(V, F, lut, cx, cy, cz);
+          if (f >= M.T) {
+            VX_DIAG(dHit);
+            hx = cx; hy = cy; hz = cz;
+            ht = t;
+            hval = f;
+            hidx = done + k + j;
+            status = kHit;
+            break;
+          }
+        }
+        if (status == kRunning) k += min(kGroup, m - k);
       }
     }
-    while (cand) {
-      const int k = __ffs(cand) - 1;
-      cand &= cand - 1;
-      const float tk = __fadd_rn(base, M.sk[k]);
-      float px = pos1(R.o[0], tk, R.d[0]);
-      float py = pos1(R.o[1], tk, R.d[1]);
-      float pz = pos1(R.o[2], tk, R.d[2]);
-      if (M.need_clip) {
-        px = clip1(px, M.xmax);
-        py = clip1(py, M.ymax);
-        pz = clip1(pz, M.zmax);
-      }
-      const int cx = __float2int_rz(px), cy = __float2int_rz(py), cz = __float2int_rz(pz);
-      const double f = filter_value<KIND, CHECKED>(V, F, lut, cx, cy, cz);
-      if (f >= M.T) {
-        hx = cx; hy = cy; hz = cz;
-        ht = tk;
-        hval = f;
-        hidx = done + k;
-        return kHit;
-      }
-    }
-    base = __fadd_rn(base, __fmul_rn((float)m, M.s));
-    done += m;
-    if (!(base <= tend)) return kMiss;
   }
-  return kExhausted;
+  return status;
 }
 
 // ---------------------------------------------------------------------------
@@ -526,9 +655,10 @@ __device__ __forceinline__ int own_budget(double te, double tx, double step) {
 // ---------------------------------------------------------------------------
 // K4
 
-template <int KIND, bool CHECKED>
+template <int KIND, bool CHECKED, bool DIAG>
 __global__ void __launch_bounds__(kTileW * kTileH) raycast_kernel(const RenderArgs a) {
   __shared__ double lut[KIND == VX_FILTER_ENTROPY ? 256 : 1];
+  __shared__ int wl[kTileW * kTileH / 32][32];
   const int tid = threadIdx.y * kTileW + threadIdx.x;
   if (KIND == VX_FILTER_ENTROPY) {
     for (int i = tid; i < 256; i += kTileW * kTileH) lut[i] = a.lut[i];
@@ -544,32 +674,46 @@ __global__ void __launch_bounds__(kTileW * kTileH) raycast_kernel(const RenderAr
   bool hit = false;
   unsigned nsamp = 0;
   uint8_t pix_out = 0;
+  Diag dg;
+  if (DIAG)
+    for (int i = 0; i < 8; ++i) dg.c[i] = 0;
+  RayState R;
+  bool live = false;
+  int limit = 0;
+  int hx = -1, hy = -1, hz = -1, hidx = 0;
+  float ht = 0.0f;
+  double hval = 0.0;
+  double d[3] = {0.0, 0.0, 0.0};
   if (valid) {
-    double d[3];
     ray_dir(a.C, i, j, d);
     double te, tx_;
     ray_span(a.C.origin, d, a.V.nx, a.V.ny, a.V.nz, te, tx_);
-    int hx = -1, hy = -1, hz = -1, hidx = 0;
-    float ht = 0.0f;
-    double hval = 0.0;
-    if (tx_ >= te && a.M.thr <= 255) {
-      RayState R;
+    hx = hy = hz = -1;
+    live = tx_ >= te && a.M.thr <= 255;
+    if (live) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         R.o[c] = __double2float_rn(__dadd_rn(a.C.origin[c], 0.5));
         R.d[c] = __double2float_rn(d[c]);
       }
+      ray_skip_consts(R);
       R.base = __double2float_rn(te);
       R.tend = __double2float_rn(tx_);
       // Per-ray budget = this ray's own max(1, ceil(span/step) + 1) <= the
       // frame-wide budget of render.py:469-473.  A ray that ends (hit or exit)
       // within it behaves exactly as under the frame budget; one that exhausts
       // it is flagged and the host re-renders with the exact frame budget.
-      const int limit = a.M.explicit_max > 0 ? a.M.explicit_max : own_budget(te, tx_, a.M.step);
-      const int st = march<KIND, CHECKED>(a.V, a.M, a.F, lut, R, limit, hx, hy, hz, ht, hval, hidx, nsamp);
-      hit = st == kHit;
-      if (st == kExhausted && a.M.explicit_max <= 0 && a.O.trunc_flag) atomicOr(a.O.trunc_flag, 1);
+      limit = a.M.explicit_max > 0 ? a.M.explicit_max : own_budget(te, tx_, a.M.step);
     }
+  }
+  // all lanes of the warp march together (cooperative sample loads)
+  {
+    const int st = march<KIND, CHECKED, DIAG>(a.V, a.M, a.F, lut, R, live, limit, hx, hy, hz, ht,
+                                              hval, hidx, nsamp, dg, wl[tid >> 5]);
+    hit = st == kHit;
+    if (st == kExhausted && a.M.explicit_max <= 0 && a.O.trunc_flag) atomicOr(a.O.trunc_flag, 1);
+  }
+  if (valid) {
     const size_t p = (size_t)j * a.C.W + i;
     uint8_t pix = (uint8_t)a.S.background;
     double I = -1.0;
@@ -599,6 +743,13 @@ __global__ void __launch_bounds__(kTileW * kTileH) raycast_kernel(const RenderAr
     unsigned s = nsamp;
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0 && s) atomicAdd(a.O.samples, (unsigned long long)s);
+  }
+  if (DIAG) {
+    for (int i = 0; i < 8; ++i) {
+      unsigned v = dg.c[i];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && v) atomicAdd(a.O.diag + i, (unsigned long long)v);
+    }
   }
   if (a.O.image_hist) {
     const unsigned key = valid ? (unsigned)pix_out : 0x100u;
@@ -639,25 +790,35 @@ __global__ void march_rays_kernel(VolView V, MarchD M, FiltD F, const double* __
                                   const int32_t* __restrict__ max_steps, int64_t n,
                                   uint8_t* hit_out, int32_t* voxel_out, float* t_out,
                                   double* value_out) {
+  __shared__ int wl[4][32];  // blockDim.x == 128
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  bool hit = false;
+  const bool valid = r < n;
   int hx = -1, hy = -1, hz = -1, hidx = 0;
   float ht = 0.0f;
   double hval = 0.0;
   unsigned nsamp = 0;
-  const double te = t_enter[r], tx = t_exit[r];
-  if (tx >= te && M.thr <= 255) {
-    RayState R;
+  RayState R;
+  bool live = false;
+  int limit = 0;
+  if (valid) {
+    const double te = t_enter[r], tx = t_exit[r];
+    live = tx >= te && M.thr <= 255;
+    if (live) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      R.o[c] = __double2float_rn(__dadd_rn(origins[3 * r + c], 0.5));
-      R.d[c] = __double2float_rn(dirs[3 * r + c]);
+      for (int c = 0; c < 3; ++c) {
+        R.o[c] = __double2float_rn(__dadd_rn(origins[3 * r + c], 0.5));
+        R.d[c] = __double2float_rn(dirs[3 * r + c]);
+      }
+      ray_skip_consts(R);
+      R.base = __double2float_rn(te);
+      R.tend = __double2float_rn(tx);
+      limit = max_steps[r];
     }
-    R.base = __double2float_rn(te);
-    R.tend = __double2float_rn(tx);
-    hit = march<KIND, CHECKED>(V, M, F, lut_g, R, max_steps[r], hx, hy, hz, ht, hval, hidx, nsamp) == kHit;
   }
+  Diag dg;
+  const bool hit = march<KIND, CHECKED, false>(V, M, F, lut_g, R, live, limit, hx, hy, hz, ht, hval,
+                                               hidx, nsamp, dg, wl[threadIdx.x >> 5]) == kHit;
+  if (!valid) return;
   hit_out[r] = hit ? 1 : 0;
   voxel_out[3 * r] = hx;
   voxel_out[3 * r + 1] = hy;
@@ -747,6 +908,8 @@ int make_march(const vx_volume* v, const vx_render_params* rp, const vx_filter_c
     return VX_EINVAL;
   }
   M.s = (float)rp->step_size;  // np.float32(step): round to nearest
+  M.inv_s = 1.0f / M.s;
+  M.sk_last = M.s * (float)(rp->chunk - 1);
   for (int k = 0; k < 16; ++k) M.sk[k] = M.s * (float)k;
   M.adv = (float)rp->chunk * M.s;
   M.xmax = (float)v->nx;
@@ -813,7 +976,10 @@ ShadeD make_shade(const vx_render_params* rp) {
 
 template <int KIND, bool CHECKED>
 void launch_raycast(const RenderArgs& a, int grid, cudaStream_t s) {
-  raycast_kernel<KIND, CHECKED><<<grid, dim3(kTileW, kTileH), 0, s>>>(a);
+  if (a.O.diag)
+    raycast_kernel<KIND, CHECKED, true><<<grid, dim3(kTileW, kTileH), 0, s>>>(a);
+  else
+    raycast_kernel<KIND, CHECKED, false><<<grid, dim3(kTileW, kTileH), 0, s>>>(a);
 }
 
 template <bool CHECKED>
@@ -898,6 +1064,7 @@ static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_p
   a.O.image_hist = reinterpret_cast<unsigned long long*>(o->image_hist);
   a.O.hit_count = reinterpret_cast<unsigned long long*>(o->hit_count);
   a.O.samples = reinterpret_cast<unsigned long long*>(o->samples);
+  a.O.diag = reinterpret_cast<unsigned long long*>(o->diag);
   a.O.trunc_flag = o->trunc_flag;
   a.world = part ? part->world : 1;
   a.rank = part ? part->rank : 0;
@@ -974,11 +1141,11 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
   const size_t o_t = out->hit_t ? take(npx * 4) : 0;
   const size_t o_val = out->hit_value ? take(npx * 8) : 0;
   const size_t o_int = out->intensity ? take(npx * 8) : 0;
-  const size_t o_small = take(256 * 8 + 3 * 8 + 8);
+  const size_t o_small = take(256 * 8 + 3 * 8 + 8 + 64);
   Scratch sc(s);
   VX_CUDA(vx_malloc_async(reinterpret_cast<uint8_t**>(&sc.p), off, s));
   uint8_t* base = sc.get<uint8_t>();
-  VX_CUDA(cudaMemsetAsync(base + o_small, 0, 256 * 8 + 3 * 8 + 8, s));
+  VX_CUDA(cudaMemsetAsync(base + o_small, 0, 256 * 8 + 3 * 8 + 8 + 64, s));
   if (part && part->world > 1) VX_CUDA(cudaMemsetAsync(base + o_pix, 0, npx, s));
   vx_render_out d;
   d.pixels = base + o_pix;
@@ -991,9 +1158,10 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
   d.hit_count = small + 256;
   d.samples = small + 257;
   d.trunc_flag = reinterpret_cast<int32_t*>(small + 258);
+  d.diag = out->diag ? small + 259 : nullptr;
   int rc = render_impl(vol, rs, rp, fc, part, &d, s, 0);
   if (rc) return rc;
-  uint64_t small_h[259];
+  uint64_t small_h[267];
   VX_CUDA(cudaMemcpyAsync(small_h, small, sizeof(small_h), cudaMemcpyDeviceToHost, s));
   VX_CUDA(cudaStreamSynchronize(s));
   int32_t flag;
@@ -1003,7 +1171,7 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
     int budget = 0;
     rc = frame_budget(vol, rs, rp->step_size, s, &budget);
     if (rc) return rc;
-    VX_CUDA(cudaMemsetAsync(small, 0, 259 * 8, s));
+    VX_CUDA(cudaMemsetAsync(small, 0, 267 * 8, s));
     rc = render_impl(vol, rs, rp, fc, part, &d, s, budget);
     if (rc) return rc;
     VX_CUDA(cudaMemcpyAsync(small_h, small, sizeof(small_h), cudaMemcpyDeviceToHost, s));
@@ -1020,6 +1188,7 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
   if (out->image_hist) memcpy(out->image_hist, small_h, 256 * 8);
   if (out->hit_count) out->hit_count[0] = small_h[256];
   if (out->samples) out->samples[0] = small_h[257];
+  if (out->diag) memcpy(out->diag, small_h + 259, 8 * 8);
   if (out->trunc_flag) out->trunc_flag[0] = 0;
   return VX_OK;
 }

@@ -40,7 +40,7 @@ __global__ void brick_max_kernel(const uint8_t* __restrict__ origin, int64_t sy,
 // D(b) = min_o max_i |b_i - o_i| over occupied o = min_oz max(|dz|, min_oy
 // max(|dy|, min_ox |dx|)).  Out-of-map cells are unoccupied; capped.
 __global__ void dist_pass_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
-                                 int mx, int my, int mz, int axis, int thr, int first) {
+                                 int mx, int my, int mz, int axis, int thr, int first, int cap) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = (int64_t)mx * my * mz;
   if (c >= n) return;
@@ -50,8 +50,8 @@ __global__ void dist_pass_kernel(const uint8_t* __restrict__ src, uint8_t* __res
   const int len = axis == 0 ? mx : (axis == 1 ? my : mz);
   const int pos = axis == 0 ? ix : (axis == 1 ? iy : iz);
   const int64_t stride = axis == 0 ? 1 : (axis == 1 ? (int64_t)mx : (int64_t)mx * my);
-  int best = VX_DIST_CAP;
-  for (int k = -VX_DIST_CAP + 1; k < VX_DIST_CAP; ++k) {
+  int best = cap;
+  for (int k = -cap + 1; k < cap; ++k) {
     const int q = pos + k;
     if (q < 0 || q >= len) continue;
     const int ak = k < 0 ? -k : k;
@@ -59,12 +59,32 @@ __global__ void dist_pass_kernel(const uint8_t* __restrict__ src, uint8_t* __res
     const uint8_t v = src[c + (int64_t)k * stride];
     int val;
     if (first)
-      val = v >= thr ? ak : VX_DIST_CAP;
+      val = v >= thr ? ak : cap;
     else
       val = v > ak ? v : ak;
     if (val < best) best = val;
   }
   dst[c] = (uint8_t)best;
+}
+
+// one thread per VX_CELL^3 cell (4^3: 4-byte aligned rows of 4 voxels)
+__global__ void cell_max_kernel(const uint8_t* __restrict__ origin, int64_t sy, int64_t sz, int ncx,
+                                int ncy, int ncz, uint8_t* __restrict__ cmax_origin, int64_t csy,
+                                int64_t csz) {
+  static_assert(VX_CELL == 4, "cell_max_kernel assumes 4^3 cells");
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= (int64_t)ncx * ncy * ncz) return;
+  const int cx = (int)(c % ncx);
+  const int cy = (int)((c / ncx) % ncy);
+  const int cz = (int)(c / ((int64_t)ncx * ncy));
+  const uint8_t* p = origin + (int64_t)cz * 4 * sz + (int64_t)cy * 4 * sy + (int64_t)cx * 4;
+  uint32_t m = 0;
+#pragma unroll
+  for (int z = 0; z < 4; ++z)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) m = __vmaxu4(m, __ldg(reinterpret_cast<const uint32_t*>(p + z * sz + y * sy)));
+  m = max(max(m & 0xffu, (m >> 8) & 0xffu), max((m >> 16) & 0xffu, m >> 24));
+  cmax_origin[(int64_t)cz * csz + (int64_t)cy * csy + cx] = (uint8_t)m;
 }
 
 __global__ void u16_to_u8_kernel(const uint16_t* __restrict__ src, uint8_t* __restrict__ dst,
@@ -155,19 +175,37 @@ int vx_launch_brick_max(vx_volume* v, cudaStream_t s) {
   return VX_OK;
 }
 
-int vx_launch_dist_map(const vx_volume* v, int thr, uint8_t* map, cudaStream_t s) {
-  const int mx = v->nbx + 2, my = v->nby + 2, mz = v->nbz + 2;
+static int dist_transform(const uint8_t* maxmap, uint8_t* out, int mx, int my, int mz, int thr,
+                          int cap, cudaStream_t s) {
   const int64_t n = (int64_t)mx * my * mz;
   uint8_t* tmp = nullptr;
   VX_CUDA(vx_malloc_async(&tmp, n, s));
   const unsigned g = (unsigned)((n + 255) / 256);
-  dist_pass_kernel<<<g, 256, 0, s>>>(v->bmax, map, mx, my, mz, 0, thr, 1);
+  dist_pass_kernel<<<g, 256, 0, s>>>(maxmap, out, mx, my, mz, 0, thr, 1, cap);
   VX_CHECK_LAUNCH();
-  dist_pass_kernel<<<g, 256, 0, s>>>(map, tmp, mx, my, mz, 1, thr, 0);
+  dist_pass_kernel<<<g, 256, 0, s>>>(out, tmp, mx, my, mz, 1, thr, 0, cap);
   VX_CHECK_LAUNCH();
-  dist_pass_kernel<<<g, 256, 0, s>>>(tmp, map, mx, my, mz, 2, thr, 0);
+  dist_pass_kernel<<<g, 256, 0, s>>>(tmp, out, mx, my, mz, 2, thr, 0, cap);
   VX_CHECK_LAUNCH();
   VX_CUDA(cudaFreeAsync(tmp, s));
+  return VX_OK;
+}
+
+// coarse (bricks) then fine (cells) Chebyshev distance maps of thr into `map`
+int vx_launch_dist_map(const vx_volume* v, int thr, uint8_t* map, cudaStream_t s) {
+  int rc = dist_transform(v->bmax, map, v->nbx + 2, v->nby + 2, v->nbz + 2, thr, VX_DIST_CAP, s);
+  if (rc) return rc;
+  return dist_transform(v->cmax, map + v->map_bytes, v->ncx + 2, v->ncy + 2, v->ncz + 2, thr,
+                        VX_FINE_CAP, s);
+}
+
+int vx_launch_cell_max(vx_volume* v, cudaStream_t s) {
+  const int64_t nc = (int64_t)v->ncx * v->ncy * v->ncz;
+  uint8_t* corigin = v->cmax + v->csz + v->csy + 1;
+  cell_max_kernel<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(v->origin, v->sy, v->sz, v->ncx,
+                                                                v->ncy, v->ncz, corigin, v->csy,
+                                                                v->csz);
+  VX_CHECK_LAUNCH();
   return VX_OK;
 }
 

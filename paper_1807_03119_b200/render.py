@@ -342,6 +342,7 @@ class FrameDetail:
     image_hist: np.ndarray
     hit_count: int
     samples: int
+    diag: dict | None = None
 
 
 def _check_render_args(config: FilterConfig, histogram, filter_fn) -> FilterConfig:
@@ -373,7 +374,9 @@ def render_detail(volume: Volume, camera: Camera, params: RenderParams, config: 
     out.hit_count = counters.ctypes.data
     out.samples = counters.ctypes.data + 8
     vox = t = val = inten = None
+    diag = np.zeros(8, dtype=np.uint64)
     if diagnostics:
+        out.diag = diag.ctypes.data
         vox = np.empty((npx, 3), dtype=np.int32)
         t = np.empty(npx, dtype=np.float32)
         val = np.empty(npx, dtype=np.float64)
@@ -387,9 +390,12 @@ def render_detail(volume: Volume, camera: Camera, params: RenderParams, config: 
         part = _lib.vx_partition(int(partition[0]), int(partition[1]))
     _lib.call("vx_render", dev.handle, C.byref(rs), C.byref(rp), C.byref(fc),
               C.byref(part) if part is not None else None, C.byref(out), exc_type=RenderError)
+    names = ("lookups", "skips", "chunks_skipped", "unused", "sample_groups",
+             "filter_evals", "hits", "iterations")
     return FrameDetail(pixels=pixels, hit_voxel=vox, hit_t=t, hit_value=val, intensity=inten,
                        image_hist=hist.astype(np.int64), hit_count=int(counters[0]),
-                       samples=int(counters[1]))
+                       samples=int(counters[1]),
+                       diag=dict(zip(names, (int(v) for v in diag))) if diagnostics else None)
 
 
 def render_frame(volume: Volume, camera: Camera, params: RenderParams, config: FilterConfig,

@@ -1,0 +1,22 @@
+"""Per-frame march statistics of the bench workload (diagnostics build path)."""
+import os, sys, time
+sys.path.insert(0, os.getcwd())
+import numpy as np
+import paper_1807_03119_b200 as vx
+from paper_1807_03119_b200 import phantoms
+from paper_1807_03119_b200.histogram import model_from_counts
+from paper_1807_03119_b200.render import render_detail
+from paper_1807_03119_b200.volume import generate_phantom_device, _attach
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+spec = phantoms.insect_phantom_spec(n)
+dev = generate_phantom_device(spec)
+h = model_from_counts(dev.counts())
+v = _attach(vx.Volume(dims=spec.dims, data=np.zeros(1, np.uint8).repeat(n**3)), dev)
+cam = vx.orbit_camera(v)
+p = vx.RenderParams(width=1024, height=1024)
+cfg = vx.FilterConfig(kind=vx.FilterKind.LOCAL_CLUSTER)
+for skip in (True,):
+    d = render_detail(v, cam, p, cfg, h, diagnostics=True, skip=skip)
+    live = int(((d.hit_voxel[:, 0] >= 0)).sum())
+    print("skip", skip, "samples", d.samples, "hits", d.hit_count, d.diag, flush=True)

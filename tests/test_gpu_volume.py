@@ -108,3 +108,13 @@ def test_distance_map_is_exact_chebyshev(vx):
     occ[1:-1, 1:-1, 1:-1] = bmax >= 100
     want = _brute_distance(occ, 24)
     assert np.array_equal(dm, want)
+    # fine level: 4^3 cells, cap 32
+    fm = dv.distance_map(100, level=1).astype(np.int64)
+    c = 4
+    ncz, ncy, ncx = (70 + c - 1) // c, (41 + c - 1) // c, (33 + c - 1) // c
+    pad2 = np.zeros((ncz * c, ncy * c, ncx * c), dtype=np.uint8)
+    pad2[:70, :41, :33] = data
+    cmax = pad2.reshape(ncz, c, ncy, c, ncx, c).max(axis=(1, 3, 5))
+    occ2 = np.zeros((ncz + 2, ncy + 2, ncx + 2), dtype=bool)
+    occ2[1:-1, 1:-1, 1:-1] = cmax >= 100
+    assert np.array_equal(fm, _brute_distance(occ2, 32))
