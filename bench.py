@@ -69,60 +69,101 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region.
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NVML (nvidia_ml_py) polled every 2 ms from a thread; falls back to
+    `nvidia-smi -lms 10` if NVML is unavailable.
+    """
+
+    REASONS = {"hw_slowdown": "nvmlClocksThrottleReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksThrottleReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksThrottleReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksThrottleReasonSwPowerCap"}
 
     def __init__(self, device: int):
         self.device = device
-        self.proc = None
-        self.lines: list[str] = []
+        self.sm: list[float] = []
+        self.max_mhz = None
+        self.reasons: set[str] = set()
+        self._stop = threading.Event()
+        self._thread = None
+        self._proc = None
+
+    def _nvml_loop(self, nv, h, masks):
+        while not self._stop.is_set():
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                for name, m in masks.items():
+                    if r & m:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
+            import pynvml as nv
+
+            nv.nvmlInit()
+            idx = self.device
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis and vis.split(",")[0].strip().isdigit():
+                idx = int(vis.split(",")[self.device])
+            h = nv.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            masks = {k: getattr(nv, v) for k, v in self.REASONS.items()}
+            self._thread = threading.Thread(target=self._nvml_loop, args=(nv, h, masks), daemon=True)
+            self._thread.start()
+            while not self.sm and self._thread.is_alive():
+                time.sleep(0.001)
         except Exception:
-            self.proc = None
+            self._start_smi()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _start_smi(self):
+        fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                  "clocks_event_reasons.hw_thermal_slowdown,"
+                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={fields}",
+                 "--format=csv,noheader,nounits", "-lms", "10"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+
+            def read():
+                names = list(self.REASONS)
+                for line in self._proc.stdout:
+                    parts = [p.strip() for p in line.split(",")]
+                    try:
+                        self.sm.append(float(parts[0]))
+                        self.max_mhz = float(parts[1])
+                    except (ValueError, IndexError):
+                        continue
+                    for n, v in zip(names, parts[2:6]):
+                        if v.lower() == "active":
+                            self.reasons.add(n)
+
+            self._thread = threading.Thread(target=read, daemon=True)
+            self._thread.start()
+            t0 = time.time()
+            while not self.sm and time.time() - t0 < 5:
+                time.sleep(0.005)
+        except Exception:
+            self._proc = None
 
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self._proc:
+            self._proc.terminate()
+        if self._thread:
+            self._thread.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in self.lines:
-            parts = [p.strip() for p in l.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx = float(parts[2])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[5:9]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.sm)}
 
 
 def cpu_baseline(volume_host: np.ndarray, cam_vec, W, H, kind, T, hist, row_step, threads):

@@ -209,6 +209,10 @@ int vx_phantom_device(uint8_t* dev_out, int64_t nx, int64_t ny, int64_t nz,
                       uint64_t noise_seed, const int64_t* spot_idx, int64_t n_spots,
                       int32_t spot_intensity, void* stream);
 
+/* ---- pinned host memory (frame outputs DMA'd without staging) ------------ */
+int vx_host_alloc(uint64_t bytes, void** out);
+int vx_host_free(void* ptr);
+
 /* ---- diagnostics ---------------------------------------------------------- */
 /* number of kernels this thread launched since the last reset */
 int vx_launch_counter(uint64_t* n_out, int reset);

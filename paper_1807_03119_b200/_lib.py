@@ -135,6 +135,8 @@ SIGNATURES = {
     "vx_volume_create_phantom": [I64, I64, I64, P, I64, F64, U64, P, I64, I32, P],
     "vx_phantom_device": [P, I64, I64, I64, P, I64, F64, U64, P, I64, I32, P],
     "vx_launch_counter": [P, C.c_int],
+    "vx_host_alloc": [U64, P],
+    "vx_host_free": [P],
     "vx_volume_distance_map": [P, I32, I32, P, P],
 }
 _RESTYPES = {"vx_last_error": C.c_char_p}
@@ -216,3 +218,36 @@ def launches(reset: bool = False) -> int:
     n = C.c_uint64(0)
     call("vx_launch_counter", C.byref(n), 1 if reset else 0)
     return int(n.value)
+
+
+class PinnedPool:
+    """Reusable page-locked host buffers for frame outputs (DMA straight into
+    the numpy arrays the caller receives; cudaHostAlloc is too slow per frame).
+    A buffer returns to the pool when the last array viewing it is freed."""
+
+    def __init__(self):
+        self._free: dict[int, list[int]] = {}
+        self._lock = threading.Lock()
+
+    def array(self, shape, dtype) -> np.ndarray:
+        dtype = np.dtype(dtype)
+        nbytes = int(np.prod(shape)) * dtype.itemsize
+        with self._lock:
+            lst = self._free.get(nbytes)
+            ptr = lst.pop() if lst else None
+        if ptr is None:
+            p = C.c_void_p()
+            call("vx_host_alloc", nbytes, C.byref(p))
+            ptr = p.value
+        buf = (C.c_uint8 * max(nbytes, 1)).from_address(ptr)
+        import weakref
+
+        weakref.finalize(buf, self._release, nbytes, ptr)
+        return np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+
+    def _release(self, nbytes, ptr):
+        with self._lock:
+            self._free.setdefault(nbytes, []).append(ptr)
+
+
+pinned = PinnedPool()

@@ -89,6 +89,20 @@ extern "C" int vx_synchronize(void) {
   return VX_OK;
 }
 
+extern "C" int vx_host_alloc(uint64_t bytes, void** out) {
+  if (!out) {
+    vx_set_error("vx_host_alloc: null argument");
+    return VX_EINVAL;
+  }
+  VX_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocDefault));
+  return VX_OK;
+}
+
+extern "C" int vx_host_free(void* p) {
+  if (p) VX_CUDA(cudaFreeHost(p));
+  return VX_OK;
+}
+
 extern "C" int vx_launch_counter(uint64_t* n_out, int reset) {
   if (n_out) *n_out = tl_launches;
   if (reset) tl_launches = 0;

@@ -24,6 +24,7 @@
 // construction; disabled automatically when thr == 0 (every brick occupied).
 
 #include <climits>
+#include <cstdlib>
 
 #include "vx_internal.cuh"
 
@@ -50,6 +51,7 @@ struct MarchD {
   int explicit_max;  // > 0: exact frame budget; 0: per-ray guard
   int thr;           // ceil(T) in [0, 255]
   int skip;
+  int skip_min_d;    // smallest cell distance that takes the box skip (tuning)
   double T;
   double step;       // FP64 step (per-ray guard)
 };
@@ -460,7 +462,7 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
           VX_DIAG(dLookup);
           const int D = __ldg(V.dist2 + (cz * (int)V.csz + cy * (int)V.csy + cx));
           float lim = -1.0f;
-          if (D >= 1) {
+          if (D >= M.skip_min_d) {
             // cells within Chebyshev distance D-1 of this one: the box
             // [4(c-D+1), 4(c+D)) per axis in p = pos + 0.5 coordinates, shrunk
             // by 1/8 voxel; the exact ray (o, d) stays inside it from t_k to
@@ -656,7 +658,7 @@ __device__ __forceinline__ int own_budget(double te, double tx, double step) {
 // K4
 
 template <int KIND, bool CHECKED, bool DIAG>
-__global__ void __launch_bounds__(kTileW * kTileH) raycast_kernel(const RenderArgs a) {
+__global__ void __launch_bounds__(kTileW * kTileH, 8) raycast_kernel(const RenderArgs a) {
   __shared__ double lut[KIND == VX_FILTER_ENTROPY ? 256 : 1];
   __shared__ int wl[kTileW * kTileH / 32][32];
   const int tid = threadIdx.y * kTileW + threadIdx.x;
@@ -683,8 +685,8 @@ __global__ void __launch_bounds__(kTileW * kTileH) raycast_kernel(const RenderAr
   int hx = -1, hy = -1, hz = -1, hidx = 0;
   float ht = 0.0f;
   double hval = 0.0;
-  double d[3] = {0.0, 0.0, 0.0};
   if (valid) {
+    double d[3];
     ray_dir(a.C, i, j, d);
     double te, tx_;
     ray_span(a.C.origin, d, a.V.nx, a.V.ny, a.V.nz, te, tx_);
@@ -718,6 +720,10 @@ __global__ void __launch_bounds__(kTileW * kTileH) raycast_kernel(const RenderAr
     uint8_t pix = (uint8_t)a.S.background;
     double I = -1.0;
     if (hit) {
+      // the FP64 direction is recomputed (bit-identical) instead of being
+      // kept live in registers across the march
+      double d[3];
+      ray_dir(a.C, i, j, d);
       const double view[3] = {-d[0], -d[1], -d[2]};
       double n[3];
       sobel<CHECKED>(a.V, hx, hy, hz, view, n);
@@ -925,6 +931,11 @@ int make_march(const vx_volume* v, const vx_render_params* rp, const vx_filter_c
   M.T = T;
   M.step = rp->step_size;
   M.skip = rp->skip && thr > 0 && thr <= 255;
+  {
+    const char* e = getenv("VOXB200_SKIP_MIN_D");
+    M.skip_min_d = e ? atoi(e) : 1;
+    if (M.skip_min_d < 1) M.skip_min_d = 1;
+  }
   return VX_OK;
 }
 
@@ -1161,30 +1172,37 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
   d.diag = out->diag ? small + 259 : nullptr;
   int rc = render_impl(vol, rs, rp, fc, part, &d, s, 0);
   if (rc) return rc;
+  // one synchronisation: counters and every requested output come back
+  // together; the rare truncation re-render (below) copies again
   uint64_t small_h[267];
-  VX_CUDA(cudaMemcpyAsync(small_h, small, sizeof(small_h), cudaMemcpyDeviceToHost, s));
-  VX_CUDA(cudaStreamSynchronize(s));
+  auto copy_back = [&]() -> int {
+    VX_CUDA(cudaMemcpyAsync(small_h, small, sizeof(small_h), cudaMemcpyDeviceToHost, s));
+    VX_CUDA(cudaMemcpyAsync(out->pixels, d.pixels, npx, cudaMemcpyDeviceToHost, s));
+    if (out->hit_voxel)
+      VX_CUDA(cudaMemcpyAsync(out->hit_voxel, d.hit_voxel, npx * 12, cudaMemcpyDeviceToHost, s));
+    if (out->hit_t) VX_CUDA(cudaMemcpyAsync(out->hit_t, d.hit_t, npx * 4, cudaMemcpyDeviceToHost, s));
+    if (out->hit_value)
+      VX_CUDA(cudaMemcpyAsync(out->hit_value, d.hit_value, npx * 8, cudaMemcpyDeviceToHost, s));
+    if (out->intensity)
+      VX_CUDA(cudaMemcpyAsync(out->intensity, d.intensity, npx * 8, cudaMemcpyDeviceToHost, s));
+    VX_CUDA(cudaStreamSynchronize(s));
+    return VX_OK;
+  };
+  rc = copy_back();
+  if (rc) return rc;
   int32_t flag;
   memcpy(&flag, &small_h[258], 4);
   if (flag && rp->max_steps <= 0) {
-    // a ray hit beyond its own span budget: re-render with the exact frame budget
+    // a ray exhausted its own span budget: re-render with the exact frame budget
     int budget = 0;
     rc = frame_budget(vol, rs, rp->step_size, s, &budget);
     if (rc) return rc;
     VX_CUDA(cudaMemsetAsync(small, 0, 267 * 8, s));
     rc = render_impl(vol, rs, rp, fc, part, &d, s, budget);
     if (rc) return rc;
-    VX_CUDA(cudaMemcpyAsync(small_h, small, sizeof(small_h), cudaMemcpyDeviceToHost, s));
+    rc = copy_back();
+    if (rc) return rc;
   }
-  VX_CUDA(cudaMemcpyAsync(out->pixels, d.pixels, npx, cudaMemcpyDeviceToHost, s));
-  if (out->hit_voxel)
-    VX_CUDA(cudaMemcpyAsync(out->hit_voxel, d.hit_voxel, npx * 12, cudaMemcpyDeviceToHost, s));
-  if (out->hit_t) VX_CUDA(cudaMemcpyAsync(out->hit_t, d.hit_t, npx * 4, cudaMemcpyDeviceToHost, s));
-  if (out->hit_value)
-    VX_CUDA(cudaMemcpyAsync(out->hit_value, d.hit_value, npx * 8, cudaMemcpyDeviceToHost, s));
-  if (out->intensity)
-    VX_CUDA(cudaMemcpyAsync(out->intensity, d.intensity, npx * 8, cudaMemcpyDeviceToHost, s));
-  VX_CUDA(cudaStreamSynchronize(s));
   if (out->image_hist) memcpy(out->image_hist, small_h, 256 * 8);
   if (out->hit_count) out->hit_count[0] = small_h[256];
   if (out->samples) out->samples[0] = small_h[257];

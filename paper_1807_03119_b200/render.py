@@ -355,17 +355,52 @@ def _check_render_args(config: FilterConfig, histogram, filter_fn) -> FilterConf
     return config
 
 
+class _StructCache:
+    """Small LRU of the packed C structs of (camera, params, config+histogram):
+    an interactive viewer re-renders with mostly unchanged state."""
+
+    def __init__(self, size: int = 32):
+        from collections import OrderedDict
+
+        self.size = size
+        self.d: OrderedDict = OrderedDict()
+
+    def get(self, key, make):
+        try:
+            v = self.d.pop(key)
+        except KeyError:
+            v = make()
+        except TypeError:  # unhashable key part
+            return make()
+        self.d[key] = v
+        if len(self.d) > self.size:
+            self.d.popitem(last=False)
+        return v
+
+
+_structs = _StructCache()
+
+
+def _native(camera, params, config, histogram, skip):
+    W, H = params.width, params.height
+    rs = _structs.get(("rs", camera, W, H), lambda: ray_setup(camera, W, H))
+    rp = _structs.get(("rp", params, skip), lambda: native_params(params, skip=skip))
+    # the histogram object is kept in the value so its id cannot be reused
+    fc = _structs.get(("fc", config, id(histogram)),
+                      lambda: (native_config(config, histogram), histogram))[0]
+    return rs, rp, fc
+
+
 def render_detail(volume: Volume, camera: Camera, params: RenderParams, config: FilterConfig,
                   histogram: HistogramModel | None = None, *, diagnostics: bool = False,
                   skip: bool = True, partition: tuple[int, int] | None = None) -> FrameDetail:
     config = _check_render_args(config, histogram, None)
     _lib.require_device()
     dev = device_volume(volume)
-    rs = ray_setup(camera, params.width, params.height)
-    rp = native_params(params, skip=skip)
-    fc = native_config(config, histogram)
+    rs, rp, fc = _native(camera, params, config, histogram, skip)
     npx = params.width * params.height
-    pixels = np.empty((params.height, params.width), dtype=np.uint8)
+    # page-locked frame: the device writes it by DMA, no staging copy
+    pixels = _lib.pinned.array((params.height, params.width), np.uint8)
     hist = np.zeros(256, dtype=np.uint64)
     counters = np.zeros(2, dtype=np.uint64)
     out = _lib.vx_render_out()
@@ -415,5 +450,5 @@ def render_frame(volume: Volume, camera: Camera, params: RenderParams, config: F
         volume_hash=volume.content_hash(),
         hit_count=d.hit_count,
     )
-    object.__setattr__(frame, "image_hist", d.image_hist)
+    frame.image_hist = d.image_hist
     return frame
