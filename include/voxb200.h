@@ -15,8 +15,10 @@
  *    vx_last_error() returns a thread-local message.
  *  - plain pointers and sizes only; "host" pointers are CPU memory, "dev"
  *    pointers are CUDA device memory of the current device.
- *  - the library is re-entrant: each calling thread gets its own CUDA stream;
- *    the only shared mutable state is per-volume caches (mutex protected).
+ *  - the library is re-entrant: each calling thread gets its own CUDA stream
+ *    for the host-buffer entry points; the *_device entry points run on the
+ *    cudaStream_t the caller passes (0 = legacy default stream).  The only
+ *    shared mutable state is per-volume caches (mutex protected).
  *  - volume layout: voxel (x, y, z) of an (nx, ny, nz) volume, x fastest,
  *    exactly the reference's `Volume.data[z, y, x]` (volume.py:3-5).
  */
@@ -149,7 +151,8 @@ int vx_histogram(vx_volume* vol, uint64_t counts_out[256]);
 /* K1 over n host bytes (uploaded) */
 int vx_histogram_host(const uint8_t* host, uint64_t n, uint64_t counts_out[256]);
 /* K1 over n device bytes, accumulating into dev_counts[256] (not zeroed),
- * asynchronously on `stream` (cudaStream_t, 0 = the calling thread's stream). */
+ * asynchronously on `stream` (a cudaStream_t used as given: 0 is the legacy default
+ * stream, so work queued by torch on its default stream is ordered before it). */
 int vx_histogram_device(const uint8_t* dev, uint64_t n, uint64_t* dev_counts, void* stream);
 /* K2: exact Otsu threshold (256-bit cross-multiplied argmin, ties -> smallest
  * T) of histogram.py:59-101; total must be < 2^47. */

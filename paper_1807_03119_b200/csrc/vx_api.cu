@@ -331,7 +331,7 @@ extern "C" int vx_phantom_device(uint8_t* dev_out, int64_t nx, int64_t ny, int64
     vx_set_error("vx_phantom_device: bad argument");
     return VX_EINVAL;
   }
-  cudaStream_t s = stream ? (cudaStream_t)stream : vx_stream();
+  cudaStream_t s = (cudaStream_t)stream;
   VX_CUDA(cudaMemsetAsync(dev_out, 0, (size_t)(nx * ny * nz), s));
   return vx_launch_phantom(dev_out, nx, nx * ny, nx, ny, nz, shapes, n_shapes, noise_sigma,
                            noise_seed, spot_idx, n_spots, spot_intensity, s);
@@ -465,7 +465,7 @@ extern "C" int vx_histogram_device(const uint8_t* dev, uint64_t n, uint64_t* dev
     vx_set_error("vx_histogram_device: null argument");
     return VX_EINVAL;
   }
-  cudaStream_t s = stream ? (cudaStream_t)stream : vx_stream();
+  cudaStream_t s = (cudaStream_t)stream;
   return vx_launch_hist(dev, n, dev_counts, s);
 }
 
@@ -499,7 +499,7 @@ extern "C" int vx_otsu_device(const uint64_t* dev_counts, int32_t* dev_T, void* 
     vx_set_error("vx_otsu_device: null argument");
     return VX_EINVAL;
   }
-  cudaStream_t s = stream ? (cudaStream_t)stream : vx_stream();
+  cudaStream_t s = (cudaStream_t)stream;
   return vx_launch_otsu(dev_counts, dev_T, s);
 }
 
@@ -539,7 +539,7 @@ extern "C" int vx_entropy_from_counts_device(const uint64_t* dev_counts, uint64_
     vx_set_error("vx_entropy_from_counts_device: null argument");
     return VX_EINVAL;
   }
-  cudaStream_t s = stream ? (cudaStream_t)stream : vx_stream();
+  cudaStream_t s = (cudaStream_t)stream;
   return vx_launch_entropy(dev_counts, n, dev_H, s);
 }
 

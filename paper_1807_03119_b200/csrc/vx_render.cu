@@ -1124,7 +1124,7 @@ static int frame_budget(vx_volume* vol, const vx_ray_setup* rs, double step, cud
 extern "C" int vx_render_device(vx_volume* vol, const vx_ray_setup* rs, const vx_render_params* rp,
                                 const vx_filter_config* fc, const vx_partition* part,
                                 vx_render_out* dev_out, void* stream) {
-  cudaStream_t s = stream ? (cudaStream_t)stream : vx_stream();
+  cudaStream_t s = (cudaStream_t)stream;
   return render_impl(vol, rs, rp, fc, part, dev_out, s, 0);
 }
 

@@ -1,0 +1,158 @@
+"""BASELINE.json configs at full size (C2 bench volume 1024^3, C4 2048^3 @2048^2,
+C5 histogram sweep up to 4096^3): parity through exact properties and
+oracle comparisons on bounded samples.  Each test keeps its host memory
+and run time bounded (a few GB, tens of seconds)."""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev_hist(t, n):
+    import torch
+
+    from paper_1807_03119_b200 import _lib
+
+    counts = torch.zeros(256, dtype=torch.int64, device=t.device)
+    s = torch.cuda.current_stream()
+    _lib.call("vx_histogram_device", C.c_void_p(t.data_ptr()), n, C.c_void_p(counts.data_ptr()),
+              C.c_void_p(s.cuda_stream))
+    torch.cuda.synchronize()
+    return counts.cpu().numpy()
+
+
+@pytest.mark.parametrize("edge", [256, 512, 1024, 2048, 4096])
+def test_c5_histogram_sweep_exact(edge):
+    """K1 at 256^3..4096^3 (68.7 GB): a byte pattern with known counts, plus
+    slab sharding (the multi-GPU split) summing to the same bins."""
+    import torch
+
+    n = edge ** 3
+    free, _ = torch.cuda.mem_get_info()
+    if n + (1 << 30) > free:
+        pytest.skip(f"{n / 1e9:.1f} GB does not fit in free device memory")
+    t = torch.empty(n, dtype=torch.uint8, device="cuda")
+    # bytes (i*37 + 11) mod 256: every level exactly n/256 times
+    pat = ((torch.arange(256, device="cuda", dtype=torch.int32) * 37 + 11) % 256).to(torch.uint8)
+    t.view(-1, 256).copy_(pat.expand(n // 256, 256))
+    counts = _dev_hist(t, n)
+    assert np.all(counts == n // 256)
+    # z-slab sharding over 8 "ranks": per-slab K1 sums to the same histogram
+    from paper_1807_03119_b200.distributed import slab_bounds
+
+    plane = edge * edge
+    tot = np.zeros(256, dtype=np.int64)
+    for r in range(8):
+        z0, z1 = slab_bounds(edge, r, 8)
+        tot += _dev_hist(t[z0 * plane:z1 * plane], (z1 - z0) * plane)
+    assert np.array_equal(tot, counts)
+    from oracle import oracle as orc
+    from paper_1807_03119_b200.histogram import otsu
+
+    assert otsu(counts) == orc.otsu(counts) == 127  # flat histogram splits in the middle
+    del t
+
+
+def test_c5_phantom_1024_vs_oracle(oracle):
+    """K1 + K2 on the 1024^3 bench phantom vs the oracle bincount of the same bytes."""
+    from paper_1807_03119_b200 import phantoms
+    from paper_1807_03119_b200.histogram import model_from_counts
+    from paper_1807_03119_b200.volume import generate_phantom_device
+
+    dev = generate_phantom_device(phantoms.insect_phantom_spec(1024))
+    host = dev.read()
+    want = oracle.hist256(host)
+    got = dev.counts()
+    assert np.array_equal(got, want)
+    assert model_from_counts(got).otsu_threshold == oracle.otsu(want)
+    dev.free()
+
+
+def test_bench_frame_1024_rows_vs_oracle(vx, oracle):
+    """The bench frame (insect 1024^3 @1024^2, local cluster): hit voxels and
+    pixels of a row sample equal the oracle's; skipping on == off everywhere."""
+    from paper_1807_03119_b200 import phantoms
+    from paper_1807_03119_b200.histogram import model_from_counts
+    from paper_1807_03119_b200.render import render_detail
+    from paper_1807_03119_b200.volume import _attach, generate_phantom_device
+
+    spec = phantoms.insect_phantom_spec(1024)
+    dev = generate_phantom_device(spec)
+    host = dev.read()
+    v = _attach(vx.Volume(dims=spec.dims, data=host), dev)
+    h = model_from_counts(dev.counts())
+    cam = vx.orbit_camera(v)
+    params = vx.RenderParams(width=1024, height=1024)
+    cfg = vx.FilterConfig(kind=vx.FilterKind.LOCAL_CLUSTER).resolve_threshold(h)
+    d = render_detail(v, cam, params, cfg, h, diagnostics=True)
+    d0 = render_detail(v, cam, params, cfg, h, diagnostics=True, skip=False)
+    assert np.array_equal(d.hit_voxel, d0.hit_voxel) and np.array_equal(d.pixels, d0.pixels)
+    assert d.samples < d0.samples / 20  # the exact skip really skips
+    step = 32
+    want = oracle.render(host, oracle.cam_vector(cam.position, cam.look_at, 1024, 1024), 1024,
+                         1024, kind="local-cluster", threshold=cfg.threshold, row_step=step,
+                         threads=oracle.max_threads())
+    rows = np.arange(0, 1024, step)
+    got_v = d.hit_voxel.reshape(1024, 1024, 3)[rows]
+    want_v = want["hit_voxel"].reshape(1024, 1024, 3)[rows]
+    assert np.array_equal(got_v, want_v)
+    assert np.array_equal(d.pixels[rows], want["pixels"][rows])
+    dev.free()
+
+
+def test_c4_2048_frame_rows_vs_oracle(vx, oracle):
+    """C4: 2048^3 CT-shaped volume, 2048^2 image (volume 8.6 GB + 9.2 GB
+    replica): a row sample of hit voxels / pixels equals the oracle's."""
+    import torch
+
+    from paper_1807_03119_b200 import phantoms
+    from paper_1807_03119_b200.histogram import model_from_counts
+    from paper_1807_03119_b200.render import render_detail
+    from paper_1807_03119_b200.volume import _attach, generate_phantom_device
+
+    free, _ = torch.cuda.mem_get_info()
+    if free < 24 << 30:
+        pytest.skip("needs ~20 GB of device memory")
+    spec = phantoms.insect_phantom_spec(2048)
+    dev = generate_phantom_device(spec)
+    host = dev.read()
+    v = _attach(vx.Volume(dims=spec.dims, data=host), dev)
+    h = model_from_counts(dev.counts())
+    assert np.array_equal(h.counts, oracle.hist256(host))
+    cam = vx.orbit_camera(v)
+    params = vx.RenderParams(width=2048, height=2048)
+    cfg = vx.FilterConfig(kind=vx.FilterKind.LOCAL_CLUSTER).resolve_threshold(h)
+    d = render_detail(v, cam, params, cfg, h, diagnostics=True)
+    step = 128
+    want = oracle.render(host, oracle.cam_vector(cam.position, cam.look_at, 2048, 2048), 2048,
+                         2048, kind="local-cluster", threshold=cfg.threshold, row_step=step,
+                         threads=oracle.max_threads())
+    rows = np.arange(0, 2048, step)
+    assert np.array_equal(d.hit_voxel.reshape(2048, 2048, 3)[rows],
+                          want["hit_voxel"].reshape(2048, 2048, 3)[rows])
+    assert np.array_equal(d.pixels[rows], want["pixels"][rows])
+    dev.free()
+
+
+def test_c4_u16_ingest_dither_roundtrip(vx, tmp_path):
+    """C4 ingestion: u16 = clamp(257*v8 + e, 0, 65535) with e in [-128, 128]
+    rescales back to v8 exactly through load_raw's device path."""
+    from paper_1807_03119_b200 import phantoms
+    from paper_1807_03119_b200.volume import generate_phantom_device
+
+    spec = phantoms.insect_phantom_spec(512)
+    dev = generate_phantom_device(spec)
+    v8 = dev.read()
+    rs = np.random.default_rng(4)
+    e = rs.integers(-128, 129, v8.shape, dtype=np.int32)
+    wide = np.clip(257 * v8.astype(np.int32) + e, 0, 65535).astype("<u2")
+    path = tmp_path / "ct.raw"
+    wide.tofile(path)
+    v = vx.load_raw(path, vx.VolumeMeta(dims=spec.dims, bit_depth=16))
+    assert np.array_equal(v.data, v8)
+    assert np.array_equal(vx.build_histogram(v).counts, dev.counts())
