@@ -373,6 +373,13 @@ __device__ __forceinline__ float clip1(float p, float hi) {
 
 enum MarchStatus { kMiss = 0, kHit = 1, kExhausted = 2 };
 
+// per-warp shared scratch of the cooperative march
+struct WarpScratch {
+  int wl[32];                // lanes needing samples, by rank
+  unsigned char items[256];  // candidate work items: (owner lane << 3) | sample j
+  unsigned char pass[256];   // filter value >= T
+};
+
 // march statistics (vx_render_out.diag); compiled in only when requested
 struct Diag {
   unsigned c[8];
@@ -423,7 +430,9 @@ __device__ __forceinline__ int first_beyond(float base, const MarchD& M, float l
 template <int KIND, bool CHECKED, bool DIAG>
 __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const double* lut,
                      const RayState& R, bool active, int limit, int& hx, int& hy, int& hz,
-                     float& ht, double& hval, int& hidx, unsigned& nsamp, Diag& dg, int* wl) {
+                     float& ht, double& hval, int& hidx, unsigned& nsamp, Diag& dg,
+                     WarpScratch* ws, bool want_value) {
+  int* wl = ws->wl;
   constexpr int kRunning = 3;
   const unsigned lane = (threadIdx.y * blockDim.x + threadIdx.x) & 31u;
   int status = active ? kRunning : kMiss;
@@ -558,36 +567,90 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
         }
       }
       __syncwarp();
-      if (need) {
-        VX_DIAG(dGroup);
-        nsamp += __popc(my_v);
-        while (my_c) {
-          const int j = __ffs(my_c) - 1;
-          my_c &= my_c - 1;
-          const float t = sample_t(base, M.s, k + j);
-          float px = pos1(R.o[0], t, R.d[0]);
-          float py = pos1(R.o[1], t, R.d[1]);
-          float pz = pos1(R.o[2], t, R.d[2]);
-          if (M.need_clip) {
-            px = clip1(px, M.xmax);
-            py = clip1(py, M.ymax);
-            pz = clip1(pz, M.zmax);
-          }
-          const int cx = __float2int_rz(px), cy = __float2int_rz(py), cz = __float2int_rz(pz);
-          VX_DIAG(dFilter);
-          const double f = filter_value<KIND, CHECKED>(V, F, lut, cx, cy, cz);
-          if (f >= M.T) {
-            VX_DIAG(dHit);
-            hx = cx; hy = cy; hz = cz;
-            ht = t;
-            hval = f;
-            hidx = done + k + j;
-            status = kHit;
-            break;
+      // ---- cooperative filter evaluation: every candidate of every needy
+      // lane is evaluated by some lane of the warp at once (filter values are
+      // pure functions of the voxel), then each owner takes its FIRST passing
+      // candidate in sample order -- the reference's sequential resolution
+      // (render.py:311-329) without serialising filter-heavy rays ----
+      const unsigned cm = need ? my_c : 0u;
+      const int nc = __popc(cm);
+        int incl = nc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if ((int)lane >= o) incl += v;
+        }
+        const int off = incl - nc;
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        {
+          unsigned c = cm;
+          int i = 0;
+          while (c) {
+            const int j = __ffs(c) - 1;
+            c &= c - 1;
+            ws->items[off + i++] = (unsigned char)((lane << 3) | j);
           }
         }
-        if (status == kRunning) k += min(kGroup, m - k);
-      }
+        __syncwarp();
+        for (int w0 = 0; w0 < total; w0 += 32) {
+          const int w = w0 + (int)lane;
+          const int item = ws->items[w < total ? w : 0];
+          const int owner = item >> 3, j = item & 7;
+          const float ob = __shfl_sync(0xffffffffu, base, owner);
+          const int okk = __shfl_sync(0xffffffffu, k, owner);
+          const float o0 = __shfl_sync(0xffffffffu, R.o[0], owner);
+          const float o1 = __shfl_sync(0xffffffffu, R.o[1], owner);
+          const float o2 = __shfl_sync(0xffffffffu, R.o[2], owner);
+          const float d0 = __shfl_sync(0xffffffffu, R.d[0], owner);
+          const float d1 = __shfl_sync(0xffffffffu, R.d[1], owner);
+          const float d2 = __shfl_sync(0xffffffffu, R.d[2], owner);
+          if (w < total) {
+            const float t = sample_t(ob, M.s, okk + j);
+            float px = pos1(o0, t, d0), py = pos1(o1, t, d1), pz = pos1(o2, t, d2);
+            if (M.need_clip) {
+              px = clip1(px, M.xmax);
+              py = clip1(py, M.ymax);
+              pz = clip1(pz, M.zmax);
+            }
+            VX_DIAG(dFilter);
+            const double f = filter_value<KIND, CHECKED>(V, F, lut, __float2int_rz(px),
+                                                         __float2int_rz(py), __float2int_rz(pz));
+            ws->pass[w] = f >= M.T ? 1 : 0;
+          }
+        }
+        __syncwarp();
+        if (need) {
+          VX_DIAG(dGroup);
+          nsamp += __popc(my_v);
+          unsigned c = cm;
+          for (int i = 0; i < nc; ++i) {
+            const int j = __ffs(c) - 1;
+            c &= c - 1;
+            if (ws->pass[off + i]) {
+              VX_DIAG(dHit);
+              const float t = sample_t(base, M.s, k + j);
+              float px = pos1(R.o[0], t, R.d[0]);
+              float py = pos1(R.o[1], t, R.d[1]);
+              float pz = pos1(R.o[2], t, R.d[2]);
+              if (M.need_clip) {
+                px = clip1(px, M.xmax);
+                py = clip1(py, M.ymax);
+                pz = clip1(pz, M.zmax);
+              }
+              hx = __float2int_rz(px);
+              hy = __float2int_rz(py);
+              hz = __float2int_rz(pz);
+              ht = t;
+              // the accepted value itself only when the caller wants it
+              if (want_value) hval = filter_value<KIND, CHECKED>(V, F, lut, hx, hy, hz);
+              hidx = done + k + j;
+              status = kHit;
+              break;
+            }
+          }
+          if (status == kRunning) k += min(kGroup, m - k);
+        }
+      __syncwarp();
     }
   }
   return status;
@@ -660,7 +723,7 @@ __device__ __forceinline__ int own_budget(double te, double tx, double step) {
 template <int KIND, bool CHECKED, bool DIAG>
 __global__ void __launch_bounds__(kTileW * kTileH, 8) raycast_kernel(const RenderArgs a) {
   __shared__ double lut[KIND == VX_FILTER_ENTROPY ? 256 : 1];
-  __shared__ int wl[kTileW * kTileH / 32][32];
+  __shared__ WarpScratch wsc[kTileW * kTileH / 32];
   const int tid = threadIdx.y * kTileW + threadIdx.x;
   if (KIND == VX_FILTER_ENTROPY) {
     for (int i = tid; i < 256; i += kTileW * kTileH) lut[i] = a.lut[i];
@@ -711,7 +774,8 @@ __global__ void __launch_bounds__(kTileW * kTileH, 8) raycast_kernel(const Rende
   // all lanes of the warp march together (cooperative sample loads)
   {
     const int st = march<KIND, CHECKED, DIAG>(a.V, a.M, a.F, lut, R, live, limit, hx, hy, hz, ht,
-                                              hval, hidx, nsamp, dg, wl[tid >> 5]);
+                                              hval, hidx, nsamp, dg, &wsc[tid >> 5],
+                                              a.O.hit_value != nullptr);
     hit = st == kHit;
     if (st == kExhausted && a.M.explicit_max <= 0 && a.O.trunc_flag) atomicOr(a.O.trunc_flag, 1);
   }
@@ -796,7 +860,7 @@ __global__ void march_rays_kernel(VolView V, MarchD M, FiltD F, const double* __
                                   const int32_t* __restrict__ max_steps, int64_t n,
                                   uint8_t* hit_out, int32_t* voxel_out, float* t_out,
                                   double* value_out) {
-  __shared__ int wl[4][32];  // blockDim.x == 128
+  __shared__ WarpScratch wsc[4];  // blockDim.x == 128
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = r < n;
   int hx = -1, hy = -1, hz = -1, hidx = 0;
@@ -823,7 +887,7 @@ __global__ void march_rays_kernel(VolView V, MarchD M, FiltD F, const double* __
   }
   Diag dg;
   const bool hit = march<KIND, CHECKED, false>(V, M, F, lut_g, R, live, limit, hx, hy, hz, ht, hval,
-                                               hidx, nsamp, dg, wl[threadIdx.x >> 5]) == kHit;
+                                               hidx, nsamp, dg, &wsc[threadIdx.x >> 5], true) == kHit;
   if (!valid) return;
   hit_out[r] = hit ? 1 : 0;
   voxel_out[3 * r] = hx;

@@ -9,14 +9,16 @@ from paper_1807_03119_b200.render import render_detail
 from paper_1807_03119_b200.volume import generate_phantom_device, _attach
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+kind = sys.argv[2] if len(sys.argv) > 2 else "local-cluster"
 spec = phantoms.insect_phantom_spec(n)
 dev = generate_phantom_device(spec)
 h = model_from_counts(dev.counts())
 v = _attach(vx.Volume(dims=spec.dims, data=np.zeros(1, np.uint8).repeat(n**3)), dev)
 cam = vx.orbit_camera(v)
 p = vx.RenderParams(width=1024, height=1024)
-cfg = vx.FilterConfig(kind=vx.FilterKind.LOCAL_CLUSTER)
+cfg = vx.FilterConfig(kind=vx.FilterKind.from_name(kind), **({"entropy_threshold": 0.5} if kind == "entropy" else {}))
 for skip in (True,):
     d = render_detail(v, cam, p, cfg, h, diagnostics=True, skip=skip)
     live = int(((d.hit_voxel[:, 0] >= 0)).sum())
-    print("skip", skip, "samples", d.samples, "hits", d.hit_count, d.diag, flush=True)
+    t0 = time.perf_counter(); d = render_detail(v, cam, p, cfg, h, diagnostics=True, skip=skip); dt = time.perf_counter() - t0
+    print(kind, n, "skip", skip, "samples", d.samples, "hits", d.hit_count, d.diag, f"{dt*1e3:.2f} ms wall", flush=True)
