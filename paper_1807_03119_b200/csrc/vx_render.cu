@@ -572,8 +572,44 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
       // pure functions of the voxel), then each owner takes its FIRST passing
       // candidate in sample order -- the reference's sequential resolution
       // (render.py:311-329) without serialising filter-heavy rays ----
-      const unsigned cm = need ? my_c : 0u;
-      const int nc = __popc(cm);
+      // ---- candidate resolution (render.py:311-329): the first candidate of
+      // each needy lane is evaluated by its owner (surface hits usually stop
+      // there); the remaining candidates of lanes whose first one failed
+      // (noise, filter-rejected interiors) are evaluated cooperatively by the
+      // whole warp -- filter values are pure functions of the voxel -- and each
+      // owner takes its FIRST passing one in sample order ----
+      if (need) {
+        VX_DIAG(dGroup);
+        nsamp += __popc(my_v);
+      }
+      unsigned rem = 0;
+      if (need && my_c) {
+        const int j = __ffs(my_c) - 1;
+        const float t = sample_t(base, M.s, k + j);
+        float px = pos1(R.o[0], t, R.d[0]);
+        float py = pos1(R.o[1], t, R.d[1]);
+        float pz = pos1(R.o[2], t, R.d[2]);
+        if (M.need_clip) {
+          px = clip1(px, M.xmax);
+          py = clip1(py, M.ymax);
+          pz = clip1(pz, M.zmax);
+        }
+        const int cx = __float2int_rz(px), cy = __float2int_rz(py), cz = __float2int_rz(pz);
+        VX_DIAG(dFilter);
+        const double f = filter_value<KIND, CHECKED>(V, F, lut, cx, cy, cz);
+        if (f >= M.T) {
+          VX_DIAG(dHit);
+          hx = cx; hy = cy; hz = cz;
+          ht = t;
+          hval = f;
+          hidx = done + k + j;
+          status = kHit;
+        } else {
+          rem = my_c & (my_c - 1);
+        }
+      }
+      if (__any_sync(0xffffffffu, rem != 0)) {
+        const int nc = __popc(rem);
         int incl = nc;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -583,7 +619,7 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
         const int off = incl - nc;
         const int total = __shfl_sync(0xffffffffu, incl, 31);
         {
-          unsigned c = cm;
+          unsigned c = rem;
           int i = 0;
           while (c) {
             const int j = __ffs(c) - 1;
@@ -619,38 +655,35 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
           }
         }
         __syncwarp();
-        if (need) {
-          VX_DIAG(dGroup);
-          nsamp += __popc(my_v);
-          unsigned c = cm;
-          for (int i = 0; i < nc; ++i) {
-            const int j = __ffs(c) - 1;
-            c &= c - 1;
-            if (ws->pass[off + i]) {
-              VX_DIAG(dHit);
-              const float t = sample_t(base, M.s, k + j);
-              float px = pos1(R.o[0], t, R.d[0]);
-              float py = pos1(R.o[1], t, R.d[1]);
-              float pz = pos1(R.o[2], t, R.d[2]);
-              if (M.need_clip) {
-                px = clip1(px, M.xmax);
-                py = clip1(py, M.ymax);
-                pz = clip1(pz, M.zmax);
-              }
-              hx = __float2int_rz(px);
-              hy = __float2int_rz(py);
-              hz = __float2int_rz(pz);
-              ht = t;
-              // the accepted value itself only when the caller wants it
-              if (want_value) hval = filter_value<KIND, CHECKED>(V, F, lut, hx, hy, hz);
-              hidx = done + k + j;
-              status = kHit;
-              break;
+        unsigned c = rem;
+        for (int i = 0; i < nc; ++i) {
+          const int j = __ffs(c) - 1;
+          c &= c - 1;
+          if (ws->pass[off + i]) {
+            VX_DIAG(dHit);
+            const float t = sample_t(base, M.s, k + j);
+            float px = pos1(R.o[0], t, R.d[0]);
+            float py = pos1(R.o[1], t, R.d[1]);
+            float pz = pos1(R.o[2], t, R.d[2]);
+            if (M.need_clip) {
+              px = clip1(px, M.xmax);
+              py = clip1(py, M.ymax);
+              pz = clip1(pz, M.zmax);
             }
+            hx = __float2int_rz(px);
+            hy = __float2int_rz(py);
+            hz = __float2int_rz(pz);
+            ht = t;
+            // the accepted value itself only when the caller wants it
+            if (want_value) hval = filter_value<KIND, CHECKED>(V, F, lut, hx, hy, hz);
+            hidx = done + k + j;
+            status = kHit;
+            break;
           }
-          if (status == kRunning) k += min(kGroup, m - k);
         }
-      __syncwarp();
+        __syncwarp();
+      }
+      if (need && status == kRunning) k += min(kGroup, m - k);
     }
   }
   return status;

@@ -68,7 +68,7 @@ def histogram_sharded(data: np.ndarray, group=None):
     z0, z1 = slab_bounds(data.shape[0], rank, world)
     dev = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.current_stream(dev)
-    slab = torch.from_numpy(np.ascontiguousarray(data[z0:z1]).reshape(-1)).to(dev)
+    slab = torch.from_numpy(np.array(data[z0:z1], copy=True).reshape(-1)).to(dev)
     counts = torch.zeros(256, dtype=torch.int64, device=dev)
     if slab.numel():
         _lib.call("vx_histogram_device", C.c_void_p(slab.data_ptr()), slab.numel(),
