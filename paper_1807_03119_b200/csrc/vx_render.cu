@@ -371,7 +371,7 @@ __device__ __forceinline__ float clip1(float p, float hi) {
   return p < 0.0f ? 0.0f : (p > hi ? hi : p);
 }
 
-enum MarchStatus { kMiss = 0, kHit = 1, kExhausted = 2 };
+enum MarchStatus { kMiss = 0, kHit = 1, kExhausted = 2, kRunning = 3 };
 
 // per-warp shared scratch of the cooperative march
 struct WarpScratch {
@@ -400,8 +400,9 @@ __device__ __forceinline__ float sample_t(float base, float s, int k) {
 // first index in [lo, m] whose sample t exceeds lim (m if none); O(1):
 // estimate, then fix up against the exact sample t (monotone in k)
 __device__ __forceinline__ int first_beyond(float base, const MarchD& M, float lim, int lo, int m) {
+  if (lo >= m) return m;
   const float q = __fmul_rn(__fsub_rn(lim, base), M.inv_s);
-  int kn = q < 0.0f ? 0 : (q >= (float)m ? m : (int)q);
+  int kn = q < 0.0f ? 0 : (q >= (float)m ? m : (int)q + 1);
   if (kn < lo) kn = lo;
   while (kn < m && sample_t(base, M.s, kn) <= lim) ++kn;
   while (kn > lo && sample_t(base, M.s, kn - 1) > lim) --kn;
@@ -427,13 +428,16 @@ __device__ __forceinline__ int first_beyond(float base, const MarchD& M, float l
 // wl: this warp's 32-int shared scratch.  All 32 lanes must call.
 // limit = the lane's sample budget.  Returns kHit, kMiss (left the span or
 // inactive) or kExhausted (budget ran out while still inside the span).
-template <int KIND, bool CHECKED, bool DIAG>
+template <int KIND, bool CHECKED, bool DIAG, bool BUDGET>
 __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const double* lut,
                      const RayState& R, bool active, int limit, int& hx, int& hy, int& hz,
                      float& ht, double& hval, int& hidx, unsigned& nsamp, Diag& dg,
                      WarpScratch* ws, bool want_value) {
+  // BUDGET: the budget `limit` caps the march exactly (render.py:293-294).
+  // !BUDGET: march unbudgeted; the caller compares the hit index with the
+  // ray's own budget (a budget can only turn a hit at index >= limit into a
+  // miss: it never changes a miss or an earlier hit).
   int* wl = ws->wl;
-  constexpr int kRunning = 3;
   const unsigned lane = (threadIdx.y * blockDim.x + threadIdx.x) & 31u;
   int status = active ? kRunning : kMiss;
   int done = 0;
@@ -441,22 +445,32 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
   float base = R.base;
   const float tend = R.tend;
   const int chunk = M.chunk;
+  // !BUDGET safety net for degenerate steps (base + adv == base): flag the
+  // ray for the exact budgeted re-render instead of looping forever
+  const int guard = BUDGET ? limit : (limit > (1 << 30) ? INT_MAX : limit + (1 << 20));
   while (__any_sync(0xffffffffu, status == kRunning)) {
     bool need = false;
-    int m = 0;
+    int m = chunk;
     if (status == kRunning) {
       VX_DIAG(dIter);
-      m = limit - done;
-      if (m > chunk) m = chunk;
+      if (BUDGET) {
+        m = limit - done;
+        if (m > chunk) m = chunk;
+      }
       if (k >= m) {  // chunk finished: exact base recurrence (render.py:331)
         base = __fadd_rn(base, __fmul_rn((float)m, M.s));
         done += m;
         k = 0;
         if (!(base <= tend))
           status = kMiss;
-        else if (done >= limit)
+        else if (done >= guard)
           status = kExhausted;
-      } else {
+        if (BUDGET && status == kRunning) {
+          m = limit - done;
+          if (m > chunk) m = chunk;
+        }
+      }
+      if (status == kRunning) {
         const float tk = sample_t(base, M.s, k);
         if (!(tk <= tend)) {
           // later samples of this chunk are beyond the exit too and the
@@ -473,12 +487,14 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
           float lim = -1.0f;
           if (D >= M.skip_min_d) {
             // cells within Chebyshev distance D-1 of this one: the box
-            // [4(c-D+1), 4(c+D)) per axis in p = pos + 0.5 coordinates, shrunk
-            // by 1/8 voxel; the exact ray (o, d) stays inside it from t_k to
-            // its exit t_box, so each sample with t <= t_box (less a t margin)
-            // truncates into an empty cell (FP32 position error < 2^-7 voxel
-            // for |p|, |t| < 8192).  Exit face per axis: 4(c+D) - 1/8 when
-            // d > 0, 4(c-D+1) + 1/8 when d < 0 (R.bo folds the offsets).
+            // [4(c-D+1), 4(c+D)) per axis in p = pos + 0.5 coordinates.  The
+            // computed positions are monotone in t on each axis, so from
+            // this sample (inside cell c) they move toward the box's far
+            // faces and cannot pass them (shrunk by 1/8 voxel; FP32 position
+            // error < 2^-7 voxel for |p|, |t| < 8192) before t_box (less a t
+            // margin): every sample up to lim truncates into an empty cell.
+            // Far face per axis: 4(c+D) - 1/8 when d > 0, 4(c-D+1) + 1/8
+            // when d < 0 (R.bo folds the offsets).
             const int cc[3] = {cx, cy, cz};
             float tb = 3.0e38f;
 #pragma unroll
@@ -493,26 +509,41 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
             // whole chunks by the exact base recurrence, then into the chunk
             // holding the first sample beyond lim
             VX_DIAG(dInChunk);
-            int lo = k + 1;  // samples before lo lie within lim
-            for (;;) {
-              k = first_beyond(base, M, lim, lo, m);
-              if (k < m) break;
+            k = first_beyond(base, M, lim, k + 1, m);
+            if (k >= m) {
               base = __fadd_rn(base, __fmul_rn((float)m, M.s));
               done += m;
-              if (!(base <= tend)) { status = kMiss; break; }
-              if (done >= limit) { status = kExhausted; break; }
-              while (done + chunk <= limit && __fadd_rn(base, M.sk_last) <= lim) {
-                VX_DIAG(dChunkLoop);
-                base = __fadd_rn(base, M.adv);
-                done += chunk;
+              k = 0;
+              if (BUDGET) {
+                // every bound of the budgeted loop (render.py:293, 331-332)
+                for (;;) {
+                  if (!(base <= tend)) { status = kMiss; break; }
+                  if (done >= limit) { status = kExhausted; break; }
+                  m = limit - done;
+                  if (m > chunk) m = chunk;
+                  if (m == chunk && __fadd_rn(base, M.sk_last) <= lim) {
+                    VX_DIAG(dChunkLoop);
+                    base = __fadd_rn(base, M.adv);
+                    done += chunk;
+                    continue;
+                  }
+                  k = first_beyond(base, M, lim, 0, m);
+                  if (k < m) break;
+                  base = __fadd_rn(base, __fmul_rn((float)m, M.s));
+                  done += m;
+                  k = 0;
+                }
+              } else {
+                // unbudgeted: full chunks; a base past the exit is caught at
+                // the next sample (t_k > tend), where the reference drops the
+                // ray too (all skipped samples are non-candidates)
+                while (__fadd_rn(base, M.sk_last) <= lim && done < guard) {
+                  VX_DIAG(dChunkLoop);
+                  base = __fadd_rn(base, M.adv);
+                  done += chunk;
+                }
+                k = first_beyond(base, M, lim, 0, chunk);
               }
-              // intermediate bases are <= this one: if it passed the exit the
-              // reference dropped the ray at the first one that did
-              if (!(base <= tend)) { status = kMiss; break; }
-              if (done >= limit) { status = kExhausted; break; }
-              m = limit - done;
-              if (m > chunk) m = chunk;
-              lo = 0;
             }
           } else {
             need = true;
@@ -753,7 +784,7 @@ __device__ __forceinline__ int own_budget(double te, double tx, double step) {
 // ---------------------------------------------------------------------------
 // K4
 
-template <int KIND, bool CHECKED, bool DIAG>
+template <int KIND, bool CHECKED, bool DIAG, bool BUDGET>
 __global__ void __launch_bounds__(kTileW * kTileH, 8) raycast_kernel(const RenderArgs a) {
   __shared__ double lut[KIND == VX_FILTER_ENTROPY ? 256 : 1];
   __shared__ WarpScratch wsc[kTileW * kTileH / 32];
@@ -806,11 +837,14 @@ __global__ void __launch_bounds__(kTileW * kTileH, 8) raycast_kernel(const Rende
   }
   // all lanes of the warp march together (cooperative sample loads)
   {
-    const int st = march<KIND, CHECKED, DIAG>(a.V, a.M, a.F, lut, R, live, limit, hx, hy, hz, ht,
-                                              hval, hidx, nsamp, dg, &wsc[tid >> 5],
-                                              a.O.hit_value != nullptr);
+    const int st = march<KIND, CHECKED, DIAG, BUDGET>(a.V, a.M, a.F, lut, R, live, limit, hx, hy,
+                                                      hz, ht, hval, hidx, nsamp, dg,
+                                                      &wsc[tid >> 5], a.O.hit_value != nullptr);
     hit = st == kHit;
-    if (st == kExhausted && a.M.explicit_max <= 0 && a.O.trunc_flag) atomicOr(a.O.trunc_flag, 1);
+    // unbudgeted march: only a hit at or beyond the ray's own budget can
+    // differ from the budgeted reference -> exact re-render by the host
+    if (!BUDGET && a.O.trunc_flag && ((hit && hidx >= limit) || st == kExhausted))
+      atomicOr(a.O.trunc_flag, 1);
   }
   if (valid) {
     const size_t p = (size_t)j * a.C.W + i;
@@ -919,7 +953,7 @@ __global__ void march_rays_kernel(VolView V, MarchD M, FiltD F, const double* __
     }
   }
   Diag dg;
-  const bool hit = march<KIND, CHECKED, false>(V, M, F, lut_g, R, live, limit, hx, hy, hz, ht, hval,
+  const bool hit = march<KIND, CHECKED, false, true>(V, M, F, lut_g, R, live, limit, hx, hy, hz, ht, hval,
                                                hidx, nsamp, dg, &wsc[threadIdx.x >> 5], true) == kHit;
   if (!valid) return;
   hit_out[r] = hit ? 1 : 0;
@@ -1084,10 +1118,13 @@ ShadeD make_shade(const vx_render_params* rp) {
 
 template <int KIND, bool CHECKED>
 void launch_raycast(const RenderArgs& a, int grid, cudaStream_t s) {
-  if (a.O.diag)
-    raycast_kernel<KIND, CHECKED, true><<<grid, dim3(kTileW, kTileH), 0, s>>>(a);
+  const dim3 blk(kTileW, kTileH);
+  if (a.M.explicit_max > 0)  // exact budget: user max_steps or the re-render
+    raycast_kernel<KIND, CHECKED, false, true><<<grid, blk, 0, s>>>(a);
+  else if (a.O.diag)
+    raycast_kernel<KIND, CHECKED, true, false><<<grid, blk, 0, s>>>(a);
   else
-    raycast_kernel<KIND, CHECKED, false><<<grid, dim3(kTileW, kTileH), 0, s>>>(a);
+    raycast_kernel<KIND, CHECKED, false, false><<<grid, blk, 0, s>>>(a);
 }
 
 template <bool CHECKED>
