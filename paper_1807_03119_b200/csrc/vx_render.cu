@@ -509,12 +509,12 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
             // whole chunks by the exact base recurrence, then into the chunk
             // holding the first sample beyond lim
             VX_DIAG(dInChunk);
-            k = first_beyond(base, M, lim, k + 1, m);
-            if (k >= m) {
-              base = __fadd_rn(base, __fmul_rn((float)m, M.s));
-              done += m;
-              k = 0;
-              if (BUDGET) {
+            if (BUDGET) {
+              k = first_beyond(base, M, lim, k + 1, m);
+              if (k >= m) {
+                base = __fadd_rn(base, __fmul_rn((float)m, M.s));
+                done += m;
+                k = 0;
                 // every bound of the budgeted loop (render.py:293, 331-332)
                 for (;;) {
                   if (!(base <= tend)) { status = kMiss; break; }
@@ -533,16 +533,32 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
                   done += m;
                   k = 0;
                 }
-              } else {
-                // unbudgeted: full chunks; a base past the exit is caught at
-                // the next sample (t_k > tend), where the reference drops the
-                // ray too (all skipped samples are non-candidates)
-                while (__fadd_rn(base, M.sk_last) <= lim && done < guard) {
-                  VX_DIAG(dChunkLoop);
+              }
+            } else {
+              // Unbudgeted: jump to a sample that is certainly <= lim (one
+              // step short of the estimate (lim - t_k)/s; FP32 rounding of
+              // sample t is far below a step), advancing whole chunks by the
+              // exact base recurrence, then walk forward to the first sample
+              // beyond lim.  A base past the exit is caught at the next sample
+              // (t_k > tend), where the reference drops the ray as well (all
+              // skipped samples are non-candidates).
+              const float q = __fmul_rn(__fsub_rn(lim, tk), M.inv_s);
+              int g = k + (q < 2.0f ? 0 : (q > 1.0e6f ? 1000000 : (int)q - 1));
+              while (g >= chunk && done < guard) {
+                VX_DIAG(dChunkLoop);
+                base = __fadd_rn(base, M.adv);
+                done += chunk;
+                g -= chunk;
+              }
+              k = g;
+              for (;;) {
+                if (k >= chunk) {
                   base = __fadd_rn(base, M.adv);
                   done += chunk;
+                  k = 0;
                 }
-                k = first_beyond(base, M, lim, 0, chunk);
+                if (sample_t(base, M.s, k) > lim || done >= guard) break;
+                ++k;
               }
             }
           } else {
