@@ -14,7 +14,7 @@ from pathlib import Path
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libvoxb200.so"
+LIB_PATH = Path(os.environ.get("VOXB200_LIB", str(_PKG / "libvoxb200.so")))
 
 VX_OK, VX_EINVAL, VX_ENOMEM, VX_ECUDA, VX_ERANGE = 0, 1, 2, 3, 5
 

@@ -648,7 +648,7 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
           VX_DIAG(dHit);
           hx = cx; hy = cy; hz = cz;
           ht = t;
-          hval = f;
+          if (want_value) hval = f;
           hidx = done + k + j;
           status = kHit;
         } else {
@@ -801,7 +801,10 @@ __device__ __forceinline__ int own_budget(double te, double tx, double step) {
 // K4
 
 template <int KIND, bool CHECKED, bool DIAG, bool BUDGET>
-__global__ void __launch_bounds__(kTileW * kTileH, 8) raycast_kernel(const RenderArgs a) {
+#ifndef VX_RAYCAST_MIN_BLOCKS
+#define VX_RAYCAST_MIN_BLOCKS 8
+#endif
+__global__ void __launch_bounds__(kTileW * kTileH, VX_RAYCAST_MIN_BLOCKS) raycast_kernel(const RenderArgs a) {
   __shared__ double lut[KIND == VX_FILTER_ENTROPY ? 256 : 1];
   __shared__ WarpScratch wsc[kTileW * kTileH / 32];
   const int tid = threadIdx.y * kTileW + threadIdx.x;

@@ -82,3 +82,23 @@ def test_timing_report(vx, small_sphere_volume, small_sphere_histogram):
     rep, _ = vx.run_entropy_comparison(v, vx.orbit_camera(v), vx.RenderParams(width=16, height=16),
                                        [vx.FilterConfig(threshold=101)], vx.build_histogram(v))
     assert rep.rows[0]["entropy_bits"] == 0.0
+
+
+def test_service_frame_message(vx, small_sphere_volume, small_sphere_histogram):
+    """§8f row 1: the framed message equals the reference's pack_frame layout
+    around the device frame (service.py:38-53, 168-183)."""
+    from paper_1807_03119_b200.frames import FRAME_HEADER, pack_frame, render_message, unpack_header
+
+    cam = vx.orbit_camera(small_sphere_volume)
+    params = vx.RenderParams(width=48, height=40)
+    cfg = vx.FilterConfig(kind=vx.FilterKind.LOCAL_CLUSTER)
+    msg = render_message(small_sphere_volume, cam, params, cfg, small_sphere_histogram, 7)
+    ref = vx.render_frame(small_sphere_volume, cam, params, cfg, small_sphere_histogram)
+    h = unpack_header(msg)
+    assert h["magic"] == b"VXSF" and h["version"] == 1 and h["sequence"] == 7
+    assert (h["width"], h["height"]) == (48, 40)
+    assert h["digest"] == ref.filter_config.digest()
+    body = bytes(msg[FRAME_HEADER.size:])
+    assert body == ref.pixels.tobytes()
+    want = pack_frame(7, 48, 40, h["render_ms"], ref.filter_config.digest(), ref.pixels.tobytes())
+    assert bytes(msg) == want

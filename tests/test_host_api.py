@@ -186,3 +186,14 @@ def test_histogram_validation_messages():
         _as_u64_counts([0] * 256)
     with pytest.raises(HistogramError, match="exact"):
         _as_u64_counts([2 ** 47] + [0] * 255)
+
+
+def test_frame_header_layout_matches_reference():
+    from paper_1807_03119_b200.frames import FRAME_HEADER, pack_frame, unpack_header
+
+    assert FRAME_HEADER.size == 32
+    m = pack_frame(3, 640, 480, 1.5, b"ABCDEFGH", b"\x01\x02")
+    h = unpack_header(m)
+    assert h == {"magic": b"VXSF", "version": 1, "sequence": 3, "width": 640, "height": 480,
+                 "render_ms": 1.5, "digest": b"ABCDEFGH"}
+    assert m[32:] == b"\x01\x02"
