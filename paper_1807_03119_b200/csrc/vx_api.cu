@@ -345,6 +345,8 @@ extern "C" int vx_volume_destroy(vx_volume* v) {
   cudaDeviceSynchronize();
   for (auto& d : v->dist)
     if (d.map) cudaFree(d.map);
+  for (auto& a : v->acc)
+    if (a.map) cudaFree(a.map);
   if (v->bmax) cudaFree(v->bmax);
   if (v->alloc) cudaFree(v->alloc);
   if (cur != v->device) cudaSetDevice(cur);

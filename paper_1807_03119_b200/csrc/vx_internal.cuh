@@ -64,6 +64,18 @@ struct DistEntry {
   uint64_t stamp;
 };
 
+// Accepted-cell distance maps: the skip structure of one filter setting.
+// Key = the filter parameters that decide `f >= T` at a voxel (opaque bytes,
+// compared exactly).  map == nullptr: the key was seen once (not built yet).
+#define VX_ACC_CACHE 4
+#define VX_ACC_KEY_BYTES 2096
+struct AccEntry {
+  bool valid = false;
+  unsigned char key[VX_ACC_KEY_BYTES];
+  uint8_t* map = nullptr;  // allocation: brick map (zeros) then cell map
+  uint64_t stamp = 0;
+};
+
 struct vx_volume {
   int nx, ny, nz;
   int device;
@@ -83,6 +95,7 @@ struct vx_volume {
   int64_t csy, csz;
   uint64_t cmap_bytes;
   DistEntry dist[VX_DIST_CACHE];
+  AccEntry acc[VX_ACC_CACHE];
   uint64_t stamp;
   uint64_t counts[256];
   std::mutex mu;
@@ -99,6 +112,10 @@ int vx_launch_entropy(const uint64_t* dev_counts, uint64_t n, double* dev_H, cud
 int vx_launch_brick_max(vx_volume* v, cudaStream_t s);
 int vx_launch_dist_map(const vx_volume* v, int thr, uint8_t* map, cudaStream_t s);
 int vx_launch_cell_max(vx_volume* v, cudaStream_t s);
+// Chebyshev cell-distance map (cap VX_FINE_CAP) of the cells whose value in
+// `occ` (cell-map layout, apron included) is >= thr
+int vx_launch_dist_cells(const vx_volume* v, const uint8_t* occ, uint8_t* out, int thr,
+                         cudaStream_t s);
 int vx_launch_u16_to_u8(const uint16_t* src, uint8_t* dst, uint64_t n, cudaStream_t s);
 int vx_launch_phantom(uint8_t* dst, int64_t row_pitch, int64_t plane_pitch, int64_t nx,
                       int64_t ny, int64_t nz, const double* shapes, int64_t n_shapes,

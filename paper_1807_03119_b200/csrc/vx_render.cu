@@ -25,6 +25,7 @@
 
 #include <climits>
 #include <cstdlib>
+#include <cstring>
 
 #include "vx_internal.cuh"
 
@@ -1177,6 +1178,89 @@ void dispatch_march(const VolView& V, const MarchD& M, const FiltD& F, const dou
 #undef VX_MR
 }
 
+// ---------------------------------------------------------------------------
+// accepted-cell occupancy (the filter-aware skip structure)
+//
+// A sample can end a ray only at a voxel v with raw(v) >= thr AND
+// filter(v) >= T (render.py:307-317): a rejected candidate is stepped over
+// exactly like an empty sample.  So the set the distance map must guard is
+// A = {v : raw >= thr, f(v) >= T}, not every candidate: isolated spots and
+// speckle that the filter rejects stop costing samples and filter
+// evaluations.  The filter is the march's own filter_value at the same
+// template arguments, so membership is bit-identical to what the march
+// would decide.  One warp per 32 cells: the lanes vote which cells hold a
+// candidate (cell max >= thr), then the warp tests such a cell's 64 voxels,
+// 32 at a time, and stops at the first accepted one.
+
+struct LutArg {
+  double v[256];
+};
+
+struct AccArgs {
+  const uint8_t* cmax;  // cell max map at cell (0,0,0)
+  uint8_t* occ;         // out: 255 where the cell holds an accepted voxel
+  int ncx, ncy, ncz;
+  int64_t csy, csz;
+  int thr;
+  double T;
+};
+
+template <int KIND, bool CHECKED>
+__global__ void __launch_bounds__(256) accept_cells_kernel(VolView V, FiltD F, AccArgs A,
+                                                           LutArg L) {
+  __shared__ double lut[KIND == VX_FILTER_ENTROPY ? 256 : 1];
+  if (KIND == VX_FILTER_ENTROPY) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = L.v[i];
+    __syncthreads();
+  }
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const long long nc = (long long)A.ncx * A.ncy * A.ncz;
+  const long long ci = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  int cx = 0, cy = 0, cz = 0;
+  bool cand = false;
+  if (ci < nc) {
+    cx = (int)(ci % A.ncx);
+    cy = (int)((ci / A.ncx) % A.ncy);
+    cz = (int)(ci / ((long long)A.ncx * A.ncy));
+    cand = __ldg(A.cmax + (cz * A.csz + cy * A.csy + cx)) >= A.thr;
+  }
+  unsigned todo = __ballot_sync(full, cand);
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const int x0 = __shfl_sync(full, cx, src) * VX_CELL;
+    const int y0 = __shfl_sync(full, cy, src) * VX_CELL;
+    const int z0 = __shfl_sync(full, cz, src) * VX_CELL;
+    bool acc = false;
+    for (int r = 0; r < 2 && !acc; ++r) {
+      const int q = r * 32 + lane;
+      const int x = x0 + (q & 3), y = y0 + ((q >> 2) & 3), z = z0 + (q >> 4);
+      bool pass = false;
+      if (x < V.nx && y < V.ny && z < V.nz && rd<false>(V, x, y, z) >= A.thr)
+        pass = filter_value<KIND, CHECKED>(V, F, lut, x, y, z) >= A.T;
+      acc = __any_sync(full, pass);
+    }
+    if (acc && lane == 0)
+      A.occ[(int64_t)(z0 >> VX_CELL_SHIFT) * A.csz + (int64_t)(y0 >> VX_CELL_SHIFT) * A.csy +
+            (x0 >> VX_CELL_SHIFT)] = 255;
+  }
+}
+
+template <bool CHECKED>
+void dispatch_accept(const VolView& V, const FiltD& F, const AccArgs& A, const LutArg& L,
+                     unsigned grid, cudaStream_t s) {
+#define VX_AC(K) accept_cells_kernel<K, CHECKED><<<grid, 256, 0, s>>>(V, F, A, L)
+  switch (F.kind) {
+    case VX_FILTER_MEAN: VX_AC(VX_FILTER_MEAN); break;
+    case VX_FILTER_SIGMA: VX_AC(VX_FILTER_SIGMA); break;
+    case VX_FILTER_OKADA: VX_AC(VX_FILTER_OKADA); break;
+    case VX_FILTER_ENTROPY: VX_AC(VX_FILTER_ENTROPY); break;
+    default: VX_AC(VX_FILTER_LOCAL_CLUSTER); break;
+  }
+#undef VX_AC
+}
+
 // scratch buffer freed on scope exit (stream ordered)
 struct Scratch {
   void* p = nullptr;
@@ -1190,6 +1274,107 @@ struct Scratch {
 };
 
 }  // namespace
+
+// Accepted-cell distance map for the render's filter setting (nullptr: use
+// the raw candidate map).  Policy: a setting seen for the first time renders
+// on the raw map (one-shot frames such as a filter comparison pay nothing);
+// from its second frame on the map is built once (~1 ms at 1024^3) and kept
+// in a small LRU on the volume.  VOXB200_ACCEPT_MAP=0 disables it, =eager
+// builds on first sight.
+static int get_accept_map(vx_volume* v, const RenderArgs& a, bool checked, const uint8_t** out,
+                          cudaStream_t s) {
+  *out = nullptr;
+  static const int mode = [] {
+    const char* e = getenv("VOXB200_ACCEPT_MAP");
+    if (!e) return 1;
+    if (!strcmp(e, "eager")) return 2;
+    return atoi(e) ? 1 : 0;
+  }();
+  if (!mode || a.F.kind == VX_FILTER_NONE || !a.M.skip) return VX_OK;
+  struct Key {
+    int32_t kind, M, d, thr;
+    double T, band, okada_t, entropy_t;
+    double lut[256];
+  } key;
+  static_assert(sizeof(Key) == VX_ACC_KEY_BYTES, "accept key layout");
+  memset(&key, 0, sizeof(key));
+  key.kind = a.F.kind;
+  key.M = a.F.M;
+  key.d = a.F.kind == VX_FILTER_LOCAL_CLUSTER ? a.F.d : 0;
+  key.thr = a.M.thr;
+  key.T = a.M.T;
+  if (a.F.kind == VX_FILTER_SIGMA) key.band = a.F.band;
+  if (a.F.kind == VX_FILTER_OKADA) key.okada_t = a.F.okada_t;
+  if (a.F.kind == VX_FILTER_ENTROPY) {
+    key.entropy_t = a.F.entropy_t;
+    memcpy(key.lut, a.lut, sizeof(key.lut));
+  }
+  std::lock_guard<std::mutex> lock(v->mu);
+  ++v->stamp;
+  AccEntry* e = nullptr;
+  for (auto& c : v->acc)
+    if (c.valid && !memcmp(c.key, &key, sizeof(key))) e = &c;
+  if (e && e->map) {
+    e->stamp = v->stamp;
+    *out = e->map;
+    return VX_OK;
+  }
+  if (!e) {
+    e = &v->acc[0];
+    for (auto& c : v->acc) {
+      if (!c.valid) {
+        e = &c;
+        break;
+      }
+      if (c.stamp < e->stamp) e = &c;
+    }
+    if (e->valid && e->map) VX_CUDA(cudaDeviceSynchronize());  // another stream may read it
+    e->valid = true;
+    memcpy(e->key, &key, sizeof(key));
+    e->stamp = v->stamp;
+    if (mode == 1) {
+      if (e->map) {
+        cudaFree(e->map);
+        e->map = nullptr;
+      }
+      return VX_OK;  // first sight: raw map
+    }
+  }
+  if (!e->map) VX_CUDA(cudaMalloc(&e->map, v->map_bytes + v->cmap_bytes));
+  e->valid = false;  // until built
+  uint8_t* occ = nullptr;
+  VX_CUDA(vx_malloc_async(&occ, v->cmap_bytes, s));
+  VX_CUDA(cudaMemsetAsync(occ, 0, v->cmap_bytes, s));
+  VX_CUDA(cudaMemsetAsync(e->map, 0, v->map_bytes, s));  // coarse level unused: no skip
+  AccArgs A;
+  A.cmax = v->cmax + v->csz + v->csy + 1;
+  A.occ = occ + v->csz + v->csy + 1;
+  A.ncx = v->ncx;
+  A.ncy = v->ncy;
+  A.ncz = v->ncz;
+  A.csy = v->csy;
+  A.csz = v->csz;
+  A.thr = a.M.thr;
+  A.T = a.M.T;
+  LutArg L;
+  memcpy(L.v, a.lut, sizeof(L.v));
+  const int64_t nc = (int64_t)v->ncx * v->ncy * v->ncz;
+  const unsigned grid = (unsigned)((nc + 255) / 256);
+  if (checked)
+    dispatch_accept<true>(a.V, a.F, A, L, grid, s);
+  else
+    dispatch_accept<false>(a.V, a.F, A, L, grid, s);
+  VX_CHECK_LAUNCH();
+  int rc = vx_launch_dist_cells(v, occ, e->map + v->map_bytes, 1, s);
+  if (rc) return rc;
+  VX_CUDA(cudaFreeAsync(occ, s));
+  // other streams may pick this map up: make it visible before publishing
+  VX_CUDA(cudaStreamSynchronize(s));
+  e->valid = true;
+  e->stamp = v->stamp;
+  *out = e->map;
+  return VX_OK;
+}
 
 // ===========================================================================
 // exported entry points
@@ -1214,9 +1399,13 @@ static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_p
   if (rc) return rc;
   a.S = make_shade(rp);
   for (int i = 0; i < 256; ++i) a.lut[i] = fc->entropy_lut[i];
+  const bool checked = filter_reach(a.F) > VX_PAD - 1;
   const uint8_t* dist = nullptr;
   if (a.M.skip) {
-    rc = vx_get_dist_map(vol, a.M.thr, &dist, s);
+    a.V = vx_view(vol, nullptr);
+    rc = get_accept_map(vol, a, checked, &dist, s);
+    if (rc) return rc;
+    if (!dist) rc = vx_get_dist_map(vol, a.M.thr, &dist, s);
     if (rc) return rc;
   }
   a.V = vx_view(vol, dist);
@@ -1241,7 +1430,6 @@ static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_p
   a.n_tiles = a.tiles_x * tiles_y;
   const int grid = (a.n_tiles - a.rank + a.world - 1) / a.world;
   if (grid <= 0) return VX_OK;
-  const bool checked = filter_reach(a.F) > VX_PAD - 1;
   if (checked)
     dispatch_raycast<true>(a, grid, s);
   else

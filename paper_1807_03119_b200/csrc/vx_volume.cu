@@ -199,6 +199,11 @@ int vx_launch_dist_map(const vx_volume* v, int thr, uint8_t* map, cudaStream_t s
                         VX_FINE_CAP, s);
 }
 
+int vx_launch_dist_cells(const vx_volume* v, const uint8_t* occ, uint8_t* out, int thr,
+                         cudaStream_t s) {
+  return dist_transform(occ, out, v->ncx + 2, v->ncy + 2, v->ncz + 2, thr, VX_FINE_CAP, s);
+}
+
 int vx_launch_cell_max(vx_volume* v, cudaStream_t s) {
   const int64_t nc = (int64_t)v->ncx * v->ncy * v->ncz;
   uint8_t* corigin = v->cmax + v->csz + v->csy + 1;

@@ -117,7 +117,11 @@ def render_sharded(volume, camera, params, config, histogram=None, group=None):
 
         d = render_detail(volume, camera, params, config, histogram, partition=(rank, world))
         pixels.copy_(torch.from_numpy(d.pixels.reshape(-1)).to(dev))
+        small[:256].copy_(torch.from_numpy(d.image_hist).to(dev))
+        small[256] = d.hit_count
+        small[258] = 0
         reduce_frame(pixels, 0, group)
+        dist.all_reduce(small, op=dist.ReduceOp.SUM, group=group)
     if rank != 0:
         return None
     frame = Frame(pixels=pixels.cpu().numpy().reshape(H, W),

@@ -17,8 +17,6 @@ v = _attach(vx.Volume(dims=spec.dims, data=np.zeros(1, np.uint8).repeat(n**3)), 
 cam = vx.orbit_camera(v)
 p = vx.RenderParams(width=1024, height=1024)
 cfg = vx.FilterConfig(kind=vx.FilterKind.from_name(kind), **({"entropy_threshold": 0.5} if kind == "entropy" else {}))
-for skip in (True,):
-    d = render_detail(v, cam, p, cfg, h, diagnostics=True, skip=skip)
-    live = int(((d.hit_voxel[:, 0] >= 0)).sum())
-    t0 = time.perf_counter(); d = render_detail(v, cam, p, cfg, h, diagnostics=True, skip=skip); dt = time.perf_counter() - t0
-    print(kind, n, "skip", skip, "samples", d.samples, "hits", d.hit_count, d.diag, f"{dt*1e3:.2f} ms wall", flush=True)
+for rep in range(3):  # raw map, accepted-cell map (built), accepted-cell map (cached)
+    t0 = time.perf_counter(); d = render_detail(v, cam, p, cfg, h, diagnostics=True); dt = time.perf_counter() - t0
+    print(kind, n, "rep", rep, "samples", d.samples, "hits", d.hit_count, d.diag, f"{dt*1e3:.2f} ms wall", flush=True)

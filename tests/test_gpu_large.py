@@ -93,6 +93,10 @@ def test_bench_frame_1024_rows_vs_oracle(vx, oracle):
     d0 = render_detail(v, cam, params, cfg, h, diagnostics=True, skip=False)
     assert np.array_equal(d.hit_voxel, d0.hit_voxel) and np.array_equal(d.pixels, d0.pixels)
     assert d.samples < d0.samples / 20  # the exact skip really skips
+    # the second frame of the setting marches on the accepted-cell map
+    d2 = render_detail(v, cam, params, cfg, h, diagnostics=True)
+    assert np.array_equal(d2.hit_voxel, d0.hit_voxel) and np.array_equal(d2.pixels, d0.pixels)
+    assert d2.diag["filter_evals"] <= d.diag["filter_evals"]
     step = 32
     want = oracle.render(host, oracle.cam_vector(cam.position, cam.look_at, 1024, 1024), 1024,
                          1024, kind="local-cluster", threshold=cfg.threshold, row_step=step,

@@ -138,7 +138,9 @@ def test_frames_match_reference(vx, name, skip):
     size = g[f"{name}__none__pixels"].shape[0]
     cam = vx.orbit_camera(v)
     params = vx.RenderParams(width=size, height=size)
-    for kind in KINDS:
+    # with skip, the second frame of a filter setting marches on its
+    # accepted-cell map (vx_render.cu get_accept_map): both must match
+    for kind, rep in [(k, r) for k in KINDS for r in range(2 if skip else 1)]:
         key = f"{name}__{kind}"
         d = render_detail(v, cam, params, cfg_for(vx, kind), h, diagnostics=True, skip=skip)
         assert np.array_equal(d.hit_voxel, g[key + "__voxel"].astype(np.int32)), key
@@ -208,7 +210,7 @@ def test_random_cameras_steps_thresholds_vs_oracle(vx, oracle):
                                  sigma_band=2.0 * h.global_sigma, probabilities=h.probabilities,
                                  entropy_threshold=cfg.entropy_threshold, step=step,
                                  max_steps=params.max_steps)
-            for skip in (True, False):
+            for skip in (True, True, False):  # raw map, accepted-cell map, no skip
                 d = render_detail(v, cam, params, cfg, h, diagnostics=True, skip=skip)
                 assert np.array_equal(d.hit_voxel, want["hit_voxel"]), (trial, kind, T, skip)
                 assert np.array_equal(d.pixels, want["pixels"]), (trial, kind, T, skip)
@@ -257,7 +259,7 @@ def test_c2_c3_frames_match_reference(vx):
     assert np.array_equal(h.counts, g["counts"]) and h.otsu_threshold == int(g["otsu"])
     cam = vx.orbit_camera(v)
     params = vx.RenderParams(width=1024, height=1024)
-    for kind in KINDS:
+    for kind, rep in [(k, r) for k in KINDS for r in range(2)]:  # raw map, accepted-cell map
         d = render_detail(v, cam, params, cfg_for(vx, kind), h, diagnostics=True)
         assert hashlib.sha256(d.hit_voxel.tobytes()).hexdigest() == str(g[f"{kind}__voxel_sha"]), kind
         assert np.array_equal(d.pixels, g[f"{kind}__pixels"]), kind
