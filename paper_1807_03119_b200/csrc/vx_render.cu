@@ -390,6 +390,10 @@ enum DiagIndex { dLookup, dInChunk, dChunkLoop, dUnused, dGroup, dFilter, dHit, 
   do {             \
     if (DIAG) ++dg.c[i]; \
   } while (0)
+#define VX_DIAG_ADD(i, v)      \
+  do {                         \
+    if (DIAG) dg.c[i] += (v);  \
+  } while (0)
 
 constexpr int kGroup = 8;  // samples loaded together in occupied regions
 
@@ -801,23 +805,34 @@ __device__ __forceinline__ int own_budget(double te, double tx, double step) {
 // ---------------------------------------------------------------------------
 // K4
 
-template <int KIND, bool CHECKED, bool DIAG, bool BUDGET>
-#ifndef VX_RAYCAST_MIN_BLOCKS
-#define VX_RAYCAST_MIN_BLOCKS 8
+// Block = kWarpsPerBlock warps, each an 8x4 pixel slab of an 8x16 tile (warps
+// retire independently; 1, 2 and 4 warps per block measured the same on the
+// bench frame, r1_config_sweep), 32 resident warps per SM.
+#ifndef VX_RAYCAST_WPB
+#define VX_RAYCAST_WPB 4
 #endif
-__global__ void __launch_bounds__(kTileW * kTileH, VX_RAYCAST_MIN_BLOCKS) raycast_kernel(const RenderArgs a) {
+#ifndef VX_RAYCAST_MIN_WARPS
+#define VX_RAYCAST_MIN_WARPS 32
+#endif
+constexpr int kWarpsPerBlock = VX_RAYCAST_WPB;
+constexpr int kBlocksPerTile = 4 / kWarpsPerBlock;
+static_assert(kWarpsPerBlock == 1 || kWarpsPerBlock == 2 || kWarpsPerBlock == 4, "warps per block");
+
+template <int KIND, bool CHECKED, bool DIAG, bool BUDGET>
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kWarpsPerBlock)
+    raycast_kernel(const RenderArgs a) {
   __shared__ double lut[KIND == VX_FILTER_ENTROPY ? 256 : 1];
-  __shared__ WarpScratch wsc[kTileW * kTileH / 32];
+  __shared__ WarpScratch wsc[kWarpsPerBlock];
   const int tid = threadIdx.y * kTileW + threadIdx.x;
   if (KIND == VX_FILTER_ENTROPY) {
-    for (int i = tid; i < 256; i += kTileW * kTileH) lut[i] = a.lut[i];
+    for (int i = tid; i < 256; i += 32 * kWarpsPerBlock) lut[i] = a.lut[i];
     __syncthreads();
   }
 
-  const int tile = a.rank + a.world * (int)blockIdx.x;
+  const int tile = a.rank + a.world * (int)(blockIdx.x / kBlocksPerTile);
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int i = tx * kTileW + threadIdx.x;
-  const int j = ty * kTileH + threadIdx.y;
+  const int j = ty * kTileH + (int)(blockIdx.x % kBlocksPerTile) * (4 * kWarpsPerBlock) + threadIdx.y;
   const bool valid = tile < a.n_tiles && i < a.C.W && j < a.C.H;
 
   bool hit = false;
@@ -1138,7 +1153,8 @@ ShadeD make_shade(const vx_render_params* rp) {
 
 template <int KIND, bool CHECKED>
 void launch_raycast(const RenderArgs& a, int grid, cudaStream_t s) {
-  const dim3 blk(kTileW, kTileH);
+  const dim3 blk(kTileW, 4 * kWarpsPerBlock);
+  grid *= kBlocksPerTile;
   if (a.M.explicit_max > 0)  // exact budget: user max_steps or the re-render
     raycast_kernel<KIND, CHECKED, false, true><<<grid, blk, 0, s>>>(a);
   else if (a.O.diag)

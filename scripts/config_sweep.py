@@ -77,6 +77,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--skip-4096", action="store_true")
+    ap.add_argument("--frames-only", action="store_true", help="skip the C5 histogram sweep")
     args = ap.parse_args()
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -106,7 +107,7 @@ def main():
     peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists(
         "MEASURED_PEAKS.json") else 6650.0
     sweep = {}
-    for edge in (256, 512, 1024, 2048, 4096):
+    for edge in (() if args.frames_only else (256, 512, 1024, 2048, 4096)):
         n = edge ** 3
         if edge == 4096 and (args.skip_4096 or torch.cuda.mem_get_info()[0] < n + (2 << 30)):
             continue
