@@ -219,10 +219,16 @@ int vx_host_free(void* ptr);
 /* ---- diagnostics ---------------------------------------------------------- */
 /* number of kernels this thread launched since the last reset */
 int vx_launch_counter(uint64_t* n_out, int reset);
+/* Frame timing of this thread's vx_render calls (Frame.timing,
+ * render.py:550-554): when on (default off: two events cost ~10 us of
+ * latency per frame), vx_last_render_ms returns the CUDA-event device time
+ * of the last frame's K4 launch(es), copy-back excluded; -1 when off. */
+int vx_set_frame_timing(int on);
+int vx_last_render_ms(float* ms_out);
 /* exact-skip structures for threshold thr, copied to host (tests):
  * level 0 = Chebyshev distance in 8^3 bricks to the nearest brick whose max
  * reaches thr (dims ceil(n/8)+2 per axis, 1-brick apron, capped at 24);
- * level 1 = the same over 2^3 cells (dims ceil(n/2)+2, capped at 8). */
+ * level 1 = the same over 4^3 cells (dims ceil(n/4)+2, capped at 32). */
 int vx_volume_distance_map(vx_volume* vol, int32_t thr, int32_t level, uint8_t* host_out,
                            int64_t dims_out[3]);
 

@@ -9,6 +9,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import threading
+import weakref
 from pathlib import Path
 
 import numpy as np
@@ -135,6 +136,8 @@ SIGNATURES = {
     "vx_volume_create_phantom": [I64, I64, I64, P, I64, F64, U64, P, I64, I32, P],
     "vx_phantom_device": [P, I64, I64, I64, P, I64, F64, U64, P, I64, I32, P],
     "vx_launch_counter": [P, C.c_int],
+    "vx_last_render_ms": [P],
+    "vx_set_frame_timing": [C.c_int],
     "vx_host_alloc": [U64, P],
     "vx_host_free": [P],
     "vx_volume_distance_map": [P, I32, I32, P, P],
@@ -230,8 +233,15 @@ class PinnedPool:
         self._lock = threading.Lock()
 
     def array(self, shape, dtype) -> np.ndarray:
+        return self.array_ptr(shape, dtype)[0]
+
+    def array_ptr(self, shape, dtype) -> tuple[np.ndarray, int]:
+        """(array, its host address)."""
         dtype = np.dtype(dtype)
-        nbytes = int(np.prod(shape)) * dtype.itemsize
+        count = 1
+        for n in shape:
+            count *= int(n)
+        nbytes = count * dtype.itemsize
         with self._lock:
             lst = self._free.get(nbytes)
             ptr = lst.pop() if lst else None
@@ -240,10 +250,8 @@ class PinnedPool:
             call("vx_host_alloc", nbytes, C.byref(p))
             ptr = p.value
         buf = (C.c_uint8 * max(nbytes, 1)).from_address(ptr)
-        import weakref
-
         weakref.finalize(buf, self._release, nbytes, ptr)
-        return np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+        return np.frombuffer(buf, dtype=dtype, count=count).reshape(shape), ptr
 
     def _release(self, nbytes, ptr):
         with self._lock:

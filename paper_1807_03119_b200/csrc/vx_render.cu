@@ -1485,6 +1485,38 @@ extern "C" int vx_render_device(vx_volume* vol, const vx_ray_setup* rs, const vx
   return render_impl(vol, rs, rp, fc, part, dev_out, s, 0);
 }
 
+// per-thread frame timing events (vx_last_render_ms)
+static thread_local cudaEvent_t tl_ev[2] = {nullptr, nullptr};
+static thread_local int tl_ev_device = -1;
+static thread_local float tl_render_ms = -1.0f;
+static thread_local bool tl_frame_timing = false;
+
+extern "C" int vx_set_frame_timing(int on) {
+  tl_frame_timing = on != 0;
+  return VX_OK;
+}
+
+extern "C" int vx_last_render_ms(float* ms_out) {
+  if (!ms_out) {
+    vx_set_error("vx_last_render_ms: null argument");
+    return VX_EINVAL;
+  }
+  *ms_out = tl_render_ms;
+  return VX_OK;
+}
+
+static int timing_events(cudaEvent_t** ev) {
+  int dev = 0;
+  VX_CUDA(cudaGetDevice(&dev));
+  if (!tl_ev[0] || tl_ev_device != dev) {
+    VX_CUDA(cudaEventCreate(&tl_ev[0]));
+    VX_CUDA(cudaEventCreate(&tl_ev[1]));
+    tl_ev_device = dev;
+  }
+  *ev = tl_ev;
+  return VX_OK;
+}
+
 extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render_params* rp,
                          const vx_filter_config* fc, const vx_partition* part, vx_render_out* out) {
   if (!vol || !rs || !rp || !fc || !out || !out->pixels) {
@@ -1527,8 +1559,18 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
   d.samples = small + 257;
   d.trunc_flag = reinterpret_cast<int32_t*>(small + 258);
   d.diag = out->diag ? small + 259 : nullptr;
-  int rc = render_impl(vol, rs, rp, fc, part, &d, s, 0);
+  const bool timed = tl_frame_timing;
+  cudaEvent_t* ev = nullptr;
+  int rc = VX_OK;
+  if (timed) {
+    rc = timing_events(&ev);
+    if (rc) return rc;
+    VX_CUDA(cudaEventRecord(ev[0], s));
+  }
+  rc = render_impl(vol, rs, rp, fc, part, &d, s, 0);
   if (rc) return rc;
+  if (timed) VX_CUDA(cudaEventRecord(ev[1], s));
+  float ms = 0.0f;
   // one synchronisation: counters and every requested output come back
   // together; the rare truncation re-render (below) copies again
   uint64_t small_h[267];
@@ -1547,6 +1589,7 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
   };
   rc = copy_back();
   if (rc) return rc;
+  if (timed) VX_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
   int32_t flag;
   memcpy(&flag, &small_h[258], 4);
   if (flag && rp->max_steps <= 0) {
@@ -1555,11 +1598,17 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
     rc = frame_budget(vol, rs, rp->step_size, s, &budget);
     if (rc) return rc;
     VX_CUDA(cudaMemsetAsync(small, 0, 267 * 8, s));
+    if (timed) VX_CUDA(cudaEventRecord(ev[0], s));
     rc = render_impl(vol, rs, rp, fc, part, &d, s, budget);
     if (rc) return rc;
+    if (timed) VX_CUDA(cudaEventRecord(ev[1], s));
     rc = copy_back();
     if (rc) return rc;
+    float ms2 = 0.0f;
+    if (timed) VX_CUDA(cudaEventElapsedTime(&ms2, ev[0], ev[1]));
+    ms += ms2;
   }
+  tl_render_ms = timed ? ms : -1.0f;
   if (out->image_hist) memcpy(out->image_hist, small_h, 256 * 8);
   if (out->hit_count) out->hit_count[0] = small_h[256];
   if (out->samples) out->samples[0] = small_h[257];

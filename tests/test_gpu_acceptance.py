@@ -74,6 +74,8 @@ def test_timing_report(vx, small_sphere_volume, small_sphere_histogram):
     t = rep.rows[0]["timing"]
     assert len(t["samples_ms"]) == 4
     assert t["median_ms"] == pytest.approx(statistics.median(t["samples_ms"]))
+    assert len(t["device_samples_ms"]) == 4 and all(0 < d for d in t["device_samples_ms"])
+    assert all(d <= w for d, w in zip(t["device_samples_ms"], t["samples_ms"]))
     assert rep.to_json()["machine"]
     with pytest.raises(ValueError):
         vx.run_entropy_comparison(small_sphere_volume, vx.orbit_camera(small_sphere_volume),

@@ -164,6 +164,14 @@ def test_render_frame_api(vx, small_sphere_volume, small_sphere_histogram):
     f = vx.render_frame(small_sphere_volume, cam, params, vx.FilterConfig(kind=vx.FilterKind.MEAN),
                         small_sphere_histogram)
     assert f.hit_count > 200 and f.pixels.shape == (64, 64) and f.timing["total_ms"] > 0
+    assert f.timing["device_ms"] is None
+    from paper_1807_03119_b200.render import frame_timing
+
+    with frame_timing():
+        f = vx.render_frame(small_sphere_volume, vx.orbit_camera(small_sphere_volume), params,
+                            vx.FilterConfig(kind=vx.FilterKind.LOCAL_CLUSTER),
+                            small_sphere_histogram)
+    assert 0 < f.timing["device_ms"] == f.timing["march_ms"] <= f.timing["total_ms"]
     frames = [vx.render_frame(small_sphere_volume, cam, params,
                               vx.FilterConfig(kind=vx.FilterKind.LOCAL_CLUSTER),
                               small_sphere_histogram, workers=w) for w in (1, 2, 5)]
