@@ -140,6 +140,20 @@ int vx_volume_create_u16(const uint16_t* host, int64_t nx, int64_t ny, int64_t n
 /* same from a device buffer (e.g. a torch tensor) */
 int vx_volume_create_device_u8(const uint8_t* dev, int64_t nx, int64_t ny, int64_t nz,
                                vx_volume** out);
+/* load_raw (volume.py:122-151) straight to the device: the headerless
+ * little-endian file is streamed through page-locked slots (file reads
+ * overlapped with the uploads), 16-bit data rescaled on the device.
+ * host_u8_out (nullable, nx*ny*nz bytes) also receives the 8-bit voxels
+ * (the reference Volume's host bytes).  Size mismatch -> VX_EINVAL with the
+ * reference's "expected N bytes ... file has M" message. */
+int vx_volume_load_raw(const char* path, int64_t nx, int64_t ny, int64_t nz, int32_t bit_depth,
+                       uint8_t* host_u8_out, vx_volume** out);
+/* load_slice_stack (volume.py:163-188) straight to the device: n_slices 8-bit
+ * PGM payloads (width*height bytes at payload_offsets[i] of paths[i], headers
+ * parsed by the caller) stacked along z. */
+int vx_volume_load_slices(const char* const* paths, const int64_t* payload_offsets,
+                          int64_t n_slices, int64_t width, int64_t height, uint8_t* host_u8_out,
+                          vx_volume** out);
 int vx_volume_destroy(vx_volume* vol);
 int vx_volume_dims(const vx_volume* vol, int64_t dims_out[3]);
 int vx_volume_read(const vx_volume* vol, uint8_t* host_out); /* compact copy back */

@@ -114,6 +114,8 @@ SIGNATURES = {
     "vx_volume_create_u8": [P, I64, I64, I64, P],
     "vx_volume_create_u16": [P, I64, I64, I64, P],
     "vx_volume_create_device_u8": [P, I64, I64, I64, P],
+    "vx_volume_load_raw": [C.c_char_p, I64, I64, I64, C.c_int32, P, P],
+    "vx_volume_load_slices": [P, P, I64, I64, I64, P, P],
     "vx_volume_destroy": [P],
     "vx_volume_dims": [P, P],
     "vx_volume_read": [P, P],

@@ -59,6 +59,52 @@ def test_slice_stack(vx, tmp_path):
     assert v.dims == (5, 6, 4) and np.array_equal(v.data, slices)
 
 
+@pytest.mark.parametrize("bits", [8, 16])
+def test_streamed_ingest_multi_chunk(vx, tmp_path, monkeypatch, bits):
+    """§8f2: the direct-to-device loader over many 1 MiB chunks (slot
+    wrap-around, u16 chunks rescaled on the device) equals numpy's load."""
+    monkeypatch.setenv("VOXB200_IO_CHUNK_MB", "1")
+    rs = np.random.default_rng(bits)
+    dims = (96, 80, 70)
+    n = dims[0] * dims[1] * dims[2]
+    if bits == 8:
+        raw = rs.integers(0, 256, n, dtype=np.uint8)
+        want = raw
+    else:
+        raw = rs.integers(0, 65536, n, dtype=np.uint32).astype("<u2")
+        want = ((raw.astype(np.int64) + 128) // 257).astype(np.uint8)
+    raw.tofile(tmp_path / "v.raw")
+    v = vx.load_raw(tmp_path / "v.raw", vx.VolumeMeta(dims=dims, bit_depth=bits))
+    assert np.array_equal(v.data.reshape(-1), want)
+    from paper_1807_03119_b200.volume import device_volume
+
+    dv = device_volume(v)
+    assert np.array_equal(dv.read().reshape(-1), want)
+    assert np.array_equal(dv.counts(), np.bincount(want, minlength=256))
+
+
+def test_streamed_slice_stack_straddles_chunks(vx, tmp_path, monkeypatch):
+    from paper_1807_03119_b200.images import write_pgm
+    from paper_1807_03119_b200.volume import VolumeError, device_volume
+
+    monkeypatch.setenv("VOXB200_IO_CHUNK_MB", "1")
+    rs = np.random.default_rng(3)
+    slices = rs.integers(0, 256, (23, 301, 197), dtype=np.uint8)  # 59 KB slices
+    for i, sl in enumerate(slices):
+        write_pgm(sl, tmp_path / f"z{i:03d}.pgm")
+    # a comment in one header moves its payload offset
+    (tmp_path / "z005.pgm").write_bytes(b"P5\n# scanner 7\n197 301\n255\n" + slices[5].tobytes())
+    v = vx.load_slice_stack(tmp_path)
+    assert v.dims == (197, 301, 23) and np.array_equal(v.data, slices)
+    assert np.array_equal(device_volume(v).read(), slices)
+    (tmp_path / "z010.pgm").write_bytes(b"P5\n197 301\n255\n" + slices[10].tobytes()[:-1])
+    with pytest.raises(VolumeError, match="payload shorter than 197x301"):
+        vx.load_slice_stack(tmp_path)
+    (tmp_path / "z010.pgm").write_bytes(b"P5\n196 301\n255\n" + slices[10].tobytes())
+    with pytest.raises(VolumeError, match="slice is 196x301, previous slices are 197x301"):
+        vx.load_slice_stack(tmp_path)
+
+
 @pytest.mark.parametrize("name", ["spot_64", "latency_64", "latency_128", "bench_128"])
 def test_device_phantom_matches_reference_bytes(vx, name):
     meta = json.loads((GOLDEN / "phantoms.json").read_text())[name]
