@@ -40,6 +40,11 @@ struct RayCamD {
   int W, H;
 };
 
+// sample-group passes whose loads are issued together (2 or 4)
+#ifndef VX_GROUP_PIPE
+#define VX_GROUP_PIPE 4
+#endif
+
 struct MarchD {
   float s;        // f32(step)
   float inv_s;    // 1/s (estimates only)
@@ -372,6 +377,21 @@ __device__ __forceinline__ float clip1(float p, float hi) {
   return p < 0.0f ? 0.0f : (p > hi ? hi : p);
 }
 
+// the voxel a sample at t truncates into (render.py:303-306), as the march
+// computes it
+__device__ __forceinline__ void voxel_at(const RayState& R, const MarchD& M, float t, int& x,
+                                         int& y, int& z) {
+  float px = pos1(R.o[0], t, R.d[0]), py = pos1(R.o[1], t, R.d[1]), pz = pos1(R.o[2], t, R.d[2]);
+  if (M.need_clip) {
+    px = clip1(px, M.xmax);
+    py = clip1(py, M.ymax);
+    pz = clip1(pz, M.zmax);
+  }
+  x = __float2int_rz(px);
+  y = __float2int_rz(py);
+  z = __float2int_rz(pz);
+}
+
 enum MarchStatus { kMiss = 0, kHit = 1, kExhausted = 2, kRunning = 3 };
 
 // per-warp shared scratch of the cooperative march
@@ -435,9 +455,12 @@ __device__ __forceinline__ int first_beyond(float base, const MarchD& M, float l
 // inactive) or kExhausted (budget ran out while still inside the span).
 template <int KIND, bool CHECKED, bool DIAG, bool BUDGET>
 __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const double* lut,
-                     const RayState& R, bool active, int limit, int& hx, int& hy, int& hz,
-                     float& ht, double& hval, int& hidx, unsigned& nsamp, Diag& dg,
-                     WarpScratch* ws, bool want_value) {
+                     const RayState& R, bool active, int limit, float& ht, int& hidx,
+                     unsigned& nsamp, Diag& dg, WarpScratch* ws) {
+  // On a hit only the sample t (ht) and its index (hidx) come back: the hit
+  // voxel is trunc(pos(ht)) and its filter value a pure function of it, so
+  // the caller recomputes both after the march (hit_voxel_of) instead of
+  // keeping six more registers live through it.
   // BUDGET: the budget `limit` caps the march exactly (render.py:293-294).
   // !BUDGET: march unbudgeted; the caller compares the hit index with the
   // ray's own budget (a budget can only turn a hit at index >= limit into a
@@ -582,7 +605,9 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
       if (need) wl[rank] = (int)lane;
       __syncwarp();
       unsigned my_c = 0, my_v = 0;
-      for (int b = 0; b < nr; b += 4) {
+      // one pass = 4 rays x 8 samples; two passes are issued back to back so
+      // their loads are in flight together
+      auto pass_load = [&](int b, int& raw, bool& inr) {
         const int q = b + (int)(lane >> 3);
         const int j = (int)(lane & 7u);
         const int src = wl[q < nr ? q : 0];  // spare slots repeat a real ray: loads stay legal
@@ -608,8 +633,10 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
           py = clip1(py, M.ymax);
           pz = clip1(pz, M.zmax);
         }
-        const int raw = rd<false>(V, __float2int_rz(px), __float2int_rz(py), __float2int_rz(pz));
-        const bool inr = q < nr && sk + j < sm && t <= st;
+        raw = rd<false>(V, __float2int_rz(px), __float2int_rz(py), __float2int_rz(pz));
+        inr = q < nr && sk + j < sm && t <= st;
+      };
+      auto pass_take = [&](int b, int raw, bool inr) {
         const unsigned bc = __ballot_sync(0xffffffffu, inr && raw >= M.thr);
         const unsigned bv = __ballot_sync(0xffffffffu, inr);
         if (need && rank >= b && rank < b + 4) {
@@ -617,7 +644,30 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
           my_c = (bc >> sh) & 0xffu;
           my_v = (bv >> sh) & 0xffu;
         }
+      };
+#if VX_GROUP_PIPE == 4
+      for (int b = 0; b < nr; b += 16) {
+        int raw0, raw1 = 0, raw2 = 0, raw3 = 0;
+        bool inr0, inr1 = false, inr2 = false, inr3 = false;
+        pass_load(b, raw0, inr0);
+        if (b + 4 < nr) pass_load(b + 4, raw1, inr1);
+        if (b + 8 < nr) pass_load(b + 8, raw2, inr2);
+        if (b + 12 < nr) pass_load(b + 12, raw3, inr3);
+        pass_take(b, raw0, inr0);
+        if (b + 4 < nr) pass_take(b + 4, raw1, inr1);
+        if (b + 8 < nr) pass_take(b + 8, raw2, inr2);
+        if (b + 12 < nr) pass_take(b + 12, raw3, inr3);
       }
+#else
+      for (int b = 0; b < nr; b += 8) {
+        int raw0, raw1 = 0;
+        bool inr0, inr1 = false;
+        pass_load(b, raw0, inr0);
+        if (b + 4 < nr) pass_load(b + 4, raw1, inr1);
+        pass_take(b, raw0, inr0);
+        if (b + 4 < nr) pass_take(b + 4, raw1, inr1);
+      }
+#endif
       __syncwarp();
       // ---- cooperative filter evaluation: every candidate of every needy
       // lane is evaluated by some lane of the warp at once (filter values are
@@ -651,10 +701,8 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
         const double f = filter_value<KIND, CHECKED>(V, F, lut, cx, cy, cz);
         if (f >= M.T) {
           VX_DIAG(dHit);
-          hx = cx; hy = cy; hz = cz;
           ht = t;
-          if (want_value) hval = f;
-          hidx = done + k + j;
+          k += j;  // hidx = done + k after the loop
           status = kHit;
         } else {
           rem = my_c & (my_c - 1);
@@ -713,22 +761,8 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
           c &= c - 1;
           if (ws->pass[off + i]) {
             VX_DIAG(dHit);
-            const float t = sample_t(base, M.s, k + j);
-            float px = pos1(R.o[0], t, R.d[0]);
-            float py = pos1(R.o[1], t, R.d[1]);
-            float pz = pos1(R.o[2], t, R.d[2]);
-            if (M.need_clip) {
-              px = clip1(px, M.xmax);
-              py = clip1(py, M.ymax);
-              pz = clip1(pz, M.zmax);
-            }
-            hx = __float2int_rz(px);
-            hy = __float2int_rz(py);
-            hz = __float2int_rz(pz);
-            ht = t;
-            // the accepted value itself only when the caller wants it
-            if (want_value) hval = filter_value<KIND, CHECKED>(V, F, lut, hx, hy, hz);
-            hidx = done + k + j;
+            ht = sample_t(base, M.s, k + j);
+            k += j;  // hidx = done + k after the loop
             status = kHit;
             break;
           }
@@ -738,6 +772,7 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
       if (need && status == kRunning) k += min(kGroup, m - k);
     }
   }
+  if (status == kHit) hidx = done + k;
   return status;
 }
 
@@ -818,6 +853,14 @@ constexpr int kWarpsPerBlock = VX_RAYCAST_WPB;
 constexpr int kBlocksPerTile = 4 / kWarpsPerBlock;
 static_assert(kWarpsPerBlock == 1 || kWarpsPerBlock == 2 || kWarpsPerBlock == 4, "warps per block");
 
+#ifdef VX_WARP_TIMING
+// debug build only: per-warp start/end globaltimer and SM of the last frame
+__device__ unsigned long long g_warp_t0[1 << 20];
+__device__ unsigned long long g_warp_t1[1 << 20];
+__device__ unsigned g_warp_sm[1 << 20];
+__device__ unsigned g_warp_diag[9 << 20];
+#endif
+
 template <int KIND, bool CHECKED, bool DIAG, bool BUDGET>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kWarpsPerBlock)
     raycast_kernel(const RenderArgs a) {
@@ -829,6 +872,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
     __syncthreads();
   }
 
+#ifdef VX_WARP_TIMING
+  unsigned long long wt0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(wt0));
+#endif
   const int tile = a.rank + a.world * (int)(blockIdx.x / kBlocksPerTile);
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int i = tx * kTileW + threadIdx.x;
@@ -872,10 +919,13 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
   }
   // all lanes of the warp march together (cooperative sample loads)
   {
-    const int st = march<KIND, CHECKED, DIAG, BUDGET>(a.V, a.M, a.F, lut, R, live, limit, hx, hy,
-                                                      hz, ht, hval, hidx, nsamp, dg,
-                                                      &wsc[tid >> 5], a.O.hit_value != nullptr);
+    const int st = march<KIND, CHECKED, DIAG, BUDGET>(a.V, a.M, a.F, lut, R, live, limit, ht,
+                                                      hidx, nsamp, dg, &wsc[tid >> 5]);
     hit = st == kHit;
+    if (hit) {
+      voxel_at(R, a.M, ht, hx, hy, hz);
+      if (a.O.hit_value) hval = filter_value<KIND, CHECKED>(a.V, a.F, lut, hx, hy, hz);
+    }
     // unbudgeted march: only a hit at or beyond the ray's own budget can
     // differ from the budgeted reference -> exact re-render by the host
     if (!BUDGET && a.O.trunc_flag && ((hit && hidx >= limit) || st == kExhausted))
@@ -921,8 +971,32 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
       unsigned v = dg.c[i];
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (lane == 0 && v) atomicAdd(a.O.diag + i, (unsigned long long)v);
+#ifdef VX_WARP_TIMING
+      const unsigned w = blockIdx.x * kWarpsPerBlock + (tid >> 5);
+      if (lane == 0 && w < (1u << 20)) g_warp_diag[w * 9 + i] = v;
+#endif
+    }
+#ifdef VX_WARP_TIMING
+    unsigned mx = dg.c[dIter];
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const unsigned w = blockIdx.x * kWarpsPerBlock + (tid >> 5);
+    if (lane == 0 && w < (1u << 20)) g_warp_diag[w * 9 + 8] = mx;
+#endif
+  }
+#ifdef VX_WARP_TIMING
+  {
+    unsigned long long wt1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(wt1));
+    const unsigned w = blockIdx.x * kWarpsPerBlock + (tid >> 5);
+    if (lane == 0 && w < (1u << 20)) {
+      g_warp_t0[w] = wt0;
+      g_warp_t1[w] = wt1;
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      g_warp_sm[w] = sm;
     }
   }
+#endif
   if (a.O.image_hist) {
     const unsigned key = valid ? (unsigned)pix_out : 0x100u;
     const unsigned peers = __match_any_sync(0xffffffffu, key);
@@ -988,8 +1062,12 @@ __global__ void march_rays_kernel(VolView V, MarchD M, FiltD F, const double* __
     }
   }
   Diag dg;
-  const bool hit = march<KIND, CHECKED, false, true>(V, M, F, lut_g, R, live, limit, hx, hy, hz, ht, hval,
-                                               hidx, nsamp, dg, &wsc[threadIdx.x >> 5], true) == kHit;
+  const bool hit = march<KIND, CHECKED, false, true>(V, M, F, lut_g, R, live, limit, ht, hidx,
+                                                     nsamp, dg, &wsc[threadIdx.x >> 5]) == kHit;
+  if (hit) {
+    voxel_at(R, M, ht, hx, hy, hz);
+    hval = filter_value<KIND, CHECKED>(V, F, lut_g, hx, hy, hz);
+  }
   if (!valid) return;
   hit_out[r] = hit ? 1 : 0;
   voxel_out[3 * r] = hx;
@@ -1815,3 +1893,21 @@ extern "C" int vx_phong_batch(const double* normals, const double* view_dirs, in
   VX_CUDA(cudaStreamSynchronize(s));
   return VX_OK;
 }
+
+#ifdef VX_WARP_TIMING
+extern "C" int vx_debug_warp_times(unsigned long long* t0, unsigned long long* t1, unsigned* sm,
+                                   int n) {
+  if (n > (1 << 20)) n = 1 << 20;
+  VX_CUDA(cudaDeviceSynchronize());
+  VX_CUDA(cudaMemcpyFromSymbol(t0, g_warp_t0, (size_t)n * 8));
+  VX_CUDA(cudaMemcpyFromSymbol(t1, g_warp_t1, (size_t)n * 8));
+  VX_CUDA(cudaMemcpyFromSymbol(sm, g_warp_sm, (size_t)n * 4));
+  return VX_OK;
+}
+extern "C" int vx_debug_warp_diag(unsigned* out, int n) {
+  if (n > (1 << 20)) n = 1 << 20;
+  VX_CUDA(cudaDeviceSynchronize());
+  VX_CUDA(cudaMemcpyFromSymbol(out, g_warp_diag, (size_t)n * 9 * 4));
+  return VX_OK;
+}
+#endif
