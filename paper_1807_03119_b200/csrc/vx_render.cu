@@ -97,6 +97,10 @@ struct RenderArgs {
   ShadeD S;
   OutD O;
   int rank, world, tiles_x, n_tiles;
+  // adaptive tile order (nullable): block b renders owned tile order[b]
+  // and records its duration in tile_cost[owned tile] for the next frame
+  const uint32_t* tile_order;
+  uint32_t* tile_cost;
   double lut[256];
 };
 
@@ -866,17 +870,26 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
     raycast_kernel(const RenderArgs a) {
   __shared__ double lut[KIND == VX_FILTER_ENTROPY ? 256 : 1];
   __shared__ WarpScratch wsc[kWarpsPerBlock];
+  __shared__ unsigned long long block_t0;
   const int tid = threadIdx.y * kTileW + threadIdx.x;
-  if (KIND == VX_FILTER_ENTROPY) {
+  if (KIND == VX_FILTER_ENTROPY)
     for (int i = tid; i < 256; i += 32 * kWarpsPerBlock) lut[i] = a.lut[i];
-    __syncthreads();
+  if (a.tile_cost && tid == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    block_t0 = t;
   }
+  if (KIND == VX_FILTER_ENTROPY || a.tile_cost) __syncthreads();
+  // owned tile of this block: the previous frame's cost order when given
+  // (heaviest first, so the longest warps start at once), else the deal
+  const int owned = a.tile_order ? (int)a.tile_order[blockIdx.x / kBlocksPerTile]
+                                 : (int)(blockIdx.x / kBlocksPerTile);
 
 #ifdef VX_WARP_TIMING
   unsigned long long wt0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(wt0));
 #endif
-  const int tile = a.rank + a.world * (int)(blockIdx.x / kBlocksPerTile);
+  const int tile = a.rank + a.world * owned;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int i = tx * kTileW + threadIdx.x;
   const int j = ty * kTileH + (int)(blockIdx.x % kBlocksPerTile) * (4 * kWarpsPerBlock) + threadIdx.y;
@@ -997,6 +1010,12 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
     }
   }
 #endif
+  if (a.tile_cost && lane == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned long long us = (t - block_t0) >> 10;  // ~microseconds
+    atomicMax(a.tile_cost + owned, (unsigned)min(us, 0xffffffffull));
+  }
   if (a.O.image_hist) {
     const unsigned key = valid ? (unsigned)pix_out : 0x100u;
     const unsigned peers = __match_any_sync(0xffffffffu, key);
@@ -1024,6 +1043,33 @@ __global__ void span_max_kernel(const RayCamD C, int nx, int ny, int nz,
     b = ob > b ? ob : b;
   }
   if ((threadIdx.x & 31) == 0) atomicMax(out_bits, b);
+}
+
+// next frame's tile order from this frame's per-tile costs: heaviest first
+// (32 log2 buckets, descending; order within a bucket is irrelevant, every
+// order renders the same frame).  One block; resets the costs.
+__global__ void __launch_bounds__(1024) tile_order_kernel(uint32_t* __restrict__ cost,
+                                                          uint32_t* __restrict__ order, int n) {
+  __shared__ unsigned cnt[33];
+  const int tid = threadIdx.x;
+  if (tid < 33) cnt[tid] = 0;
+  __syncthreads();
+  for (int i = tid; i < n; i += blockDim.x) atomicAdd(&cnt[31 - __clz(cost[i] | 1u)], 1u);
+  __syncthreads();
+  if (tid == 0) {
+    unsigned run = 0;
+    for (int b = 31; b >= 0; --b) {
+      const unsigned c = cnt[b];
+      cnt[b] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += blockDim.x) {
+    const unsigned b = 31 - __clz(cost[i] | 1u);
+    order[atomicAdd(&cnt[b], 1u)] = (uint32_t)i;
+    cost[i] = 0;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1473,6 +1519,53 @@ static int get_accept_map(vx_volume* v, const RenderArgs& a, bool checked, const
 // ===========================================================================
 // exported entry points
 
+// Adaptive tile order: K4 records each tile's duration; a one-block kernel
+// turns them into the next frame's order, heaviest first, so the longest
+// warps (rays threading cluttered free space) start at once instead of
+// setting the frame's tail.  Any order renders the same frame (tiles are
+// independent), so stale costs only cost time.  Per calling thread, keyed by
+// (volume, frame size, partition, stream); VOXB200_TILE_ORDER=0 disables.
+struct TileSched {
+  const void* vol = nullptr;
+  int w = 0, h = 0, rank = 0, world = 0, grid = 0;
+  cudaStream_t stream = nullptr;
+  uint32_t* buf = nullptr;  // order[grid] then cost[grid]
+  bool valid = false;
+};
+static thread_local TileSched tl_sched;
+
+static int tile_sched(vx_volume* vol, const vx_ray_setup* rs, int rank, int world, int grid,
+                      cudaStream_t s, TileSched** out) {
+  static const bool enabled = [] {
+    const char* e = getenv("VOXB200_TILE_ORDER");
+    return !e || atoi(e) != 0;
+  }();
+  *out = nullptr;
+  // small frames fit in one wave of blocks: nothing to reorder
+  if (!enabled || grid < 4 * vx_sm_count()) return VX_OK;
+  TileSched& t = tl_sched;
+  if (t.vol != vol || t.w != rs->width || t.h != rs->height || t.rank != rank ||
+      t.world != world || t.grid != grid || t.stream != s || !t.buf) {
+    if (t.buf) {
+      VX_CUDA(cudaStreamSynchronize(t.stream));
+      VX_CUDA(cudaFree(t.buf));
+      t.buf = nullptr;
+    }
+    VX_CUDA(cudaMalloc(&t.buf, (size_t)grid * 8));
+    VX_CUDA(cudaMemsetAsync(t.buf + grid, 0, (size_t)grid * 4, s));
+    t.vol = vol;
+    t.w = rs->width;
+    t.h = rs->height;
+    t.rank = rank;
+    t.world = world;
+    t.grid = grid;
+    t.stream = s;
+    t.valid = false;
+  }
+  *out = &t;
+  return VX_OK;
+}
+
 static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_params* rp,
                        const vx_filter_config* fc, const vx_partition* part, vx_render_out* o,
                        cudaStream_t s, int explicit_budget_override) {
@@ -1524,11 +1617,25 @@ static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_p
   a.n_tiles = a.tiles_x * tiles_y;
   const int grid = (a.n_tiles - a.rank + a.world - 1) / a.world;
   if (grid <= 0) return VX_OK;
+  TileSched* ts = nullptr;
+  a.tile_order = nullptr;
+  a.tile_cost = nullptr;
+  rc = tile_sched(vol, rs, a.rank, a.world, grid, s, &ts);
+  if (rc) return rc;
+  if (ts) {
+    a.tile_cost = ts->buf + grid;
+    a.tile_order = ts->valid ? ts->buf : nullptr;
+  }
   if (checked)
     dispatch_raycast<true>(a, grid, s);
   else
     dispatch_raycast<false>(a, grid, s);
   VX_CHECK_LAUNCH();
+  if (ts) {
+    tile_order_kernel<<<1, 1024, 0, s>>>(ts->buf + grid, ts->buf, grid);
+    VX_CHECK_LAUNCH();
+    ts->valid = true;
+  }
   return VX_OK;
 }
 
