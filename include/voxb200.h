@@ -238,6 +238,16 @@ int vx_launch_counter(uint64_t* n_out, int reset);
  * latency per frame), vx_last_render_ms returns the CUDA-event device time
  * of the last frame's K4 launch(es), copy-back excluded; -1 when off. */
 int vx_set_frame_timing(int on);
+/* K4 scheduling (process-wide; results never depend on it): tile_order 1/0
+ * (-1: env VOXB200_TILE_ORDER, default on) reorders a frame's 8x16 tiles by
+ * the previous frame's per-tile cost, heaviest first, for frames of at least
+ * min_grid_tiles tiles (-1: 4 per SM).  The tiles that would outlast the
+ * frame's ideal length (total cost / concurrent tile slots), when the
+ * heaviest took >= split_min_us, are rendered with every ray split into two
+ * segments on two lanes (at most grid / split_max_div tiles; split_min_us 0
+ * splits every tile; the entropy filter is not split by default). */
+int vx_set_schedule(int32_t tile_order, int32_t min_grid_tiles, int32_t split_min_us,
+                    int32_t split_max_div);
 int vx_last_render_ms(float* ms_out);
 /* exact-skip structures for threshold thr, copied to host (tests):
  * level 0 = Chebyshev distance in 8^3 bricks to the nearest brick whose max

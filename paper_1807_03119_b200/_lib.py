@@ -140,6 +140,7 @@ SIGNATURES = {
     "vx_launch_counter": [P, C.c_int],
     "vx_last_render_ms": [P],
     "vx_set_frame_timing": [C.c_int],
+    "vx_set_schedule": [C.c_int32, C.c_int32, C.c_int32, C.c_int32],
     "vx_host_alloc": [U64, P],
     "vx_host_free": [P],
     "vx_volume_distance_map": [P, I32, I32, P, P],

@@ -4,7 +4,7 @@
 mkdir -p gpurun_out
 for v in "$@"; do
   echo "== lib$v"
-  VOXB200_LIB=$PWD/paper_1807_03119_b200/libvoxb200$v.so VOXB200_NO_BUILD=1 timeout 600 \
+  VOXB200_LIB=$PWD/paper_1807_03119_b200/libvoxb200$v.so VOXB200_NO_BUILD=1 timeout ${SWEEP_TIMEOUT:-180} \
     python scripts/config_sweep.py --frames-only --reps 20 > gpurun_out/sweep$v.json 2>gpurun_out/sweep$v.err
   python - "$v" <<'PY'
 import json, sys

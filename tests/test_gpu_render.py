@@ -321,3 +321,48 @@ def test_sharded_api_single_rank_nccl(vx, small_sphere_volume, small_sphere_hist
         assert np.array_equal(f.image_hist, np.bincount(ref.pixels.reshape(-1), minlength=256))
     finally:
         dist.destroy_process_group()
+
+
+@pytest.fixture
+def split_everything():
+    """Schedule every frame's tiles by cost and split every ray of every tile
+    in two segments (production only splits the heaviest tiles of big
+    frames); restored afterwards."""
+    from paper_1807_03119_b200 import _lib
+
+    _lib.call("vx_set_schedule", 1, 0, 0, 1)
+    yield
+    _lib.call("vx_set_schedule", -1, -1, 16, 8)
+
+
+def test_split_rays_and_tile_order_match_oracle(vx, oracle, split_everything):
+    """Frames 2+ of a setting run with the cost-ordered tiles and two-segment
+    rays (segment 1 starts from the exact chunk base of its first sample):
+    hit voxels and pixels equal the oracle's, for every filter and steps that
+    exercise the chunk rule."""
+    from paper_1807_03119_b200.render import render_detail
+
+    rs = np.random.default_rng(11)
+    data = (rs.random((48, 40, 56)) < 0.03).astype(np.uint8) * 230 + rs.integers(
+        0, 60, (48, 40, 56), dtype=np.uint8)
+    data[8:30, 10:30, 12:40] = np.maximum(data[8:30, 10:30, 12:40], 160)
+    v = vol_from(vx, data)
+    h = vx.build_histogram(v)
+    for trial, step in enumerate([0.5, 0.37, 1.0, 2.5]):
+        pos = tuple(float(x) for x in rs.uniform(-90, 150, 3))
+        look = tuple(float(x) for x in rs.uniform(5, 40, 3))
+        cam = vx.Camera(position=pos, look_at=look, fov_y_deg=float(rs.uniform(20, 70)))
+        w, hh = int(rs.integers(40, 90)), int(rs.integers(40, 90))
+        params = vx.RenderParams(width=w, height=hh, step_size=step)
+        cv = oracle.cam_vector(pos, look, w, hh, fov_y_deg=cam.fov_y_deg)
+        for kind in KINDS:
+            T = float(rs.choice([40.5, 67.0, 149.0]))
+            cfg = cfg_for(vx, kind, threshold=T)
+            want = oracle.render(data, cv, w, hh, kind=kind, threshold=T,
+                                 sigma_band=2.0 * h.global_sigma, probabilities=h.probabilities,
+                                 entropy_threshold=cfg.entropy_threshold, step=step)
+            for rep in range(3):
+                d = render_detail(v, cam, params, cfg, h, diagnostics=rep == 2)
+                assert np.array_equal(d.pixels, want["pixels"]), (trial, kind, T, rep)
+                if rep == 2:
+                    assert np.array_equal(d.hit_voxel, want["hit_voxel"]), (trial, kind, T)
