@@ -46,7 +46,7 @@ b = np.arange(nw) // 4
 ty, tx = b // tiles_x, b % tiles_x
 row = ty * 16 + (np.arange(nw) % 4) * 4
 col = tx * 8
-top = np.argsort(-dur)[:12]
+top = np.argsort(-dur)[:6]
 for w in top:
     print(f"  warp {w}: dur {dur[w]:.1f} us start {s[w]:.1f} rows {row[w]}..{row[w]+3} cols {col[w]}..{col[w]+7} sm {sm[w]}")
 # duration by image band (64 rows)
