@@ -241,11 +241,12 @@ int vx_set_frame_timing(int on);
 /* K4 scheduling (process-wide; results never depend on it): tile_order 1/0
  * (-1: env VOXB200_TILE_ORDER, default on) reorders a frame's 8x16 tiles by
  * the previous frame's per-tile cost, heaviest first, for frames of at least
- * min_grid_tiles tiles (-1: 4 per SM).  The tiles that would outlast the
- * frame's ideal length (total cost / concurrent tile slots), when the
- * heaviest took >= split_min_us, are rendered with every ray split into two
- * segments on two lanes (at most grid / split_max_div tiles; split_min_us 0
- * splits every tile; the entropy filter is not split by default). */
+ * min_grid_tiles tiles (-1: 4 per SM).  Tiles that would outlast the frame's
+ * ideal length (total cost / concurrent tile slots) are rendered with every
+ * ray split into 2 segments on 2 lanes, twice that length into 4, when the
+ * heaviest took >= split_min_us; at most grid / split_max_div extra blocks
+ * (split_min_us 0: a quarter of the tiles split in 4 and a quarter in 2,
+ * for tests; the entropy filter is not split by default). */
 int vx_set_schedule(int32_t tile_order, int32_t min_grid_tiles, int32_t split_min_us,
                     int32_t split_max_div);
 int vx_last_render_ms(float* ms_out);

@@ -891,21 +891,31 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
   const int tid = threadIdx.y * kTileW + threadIdx.x;
   // owned tile of this block: the previous frame's cost order when given
   // (heaviest first, so the longest warps start at once), else the deal.
-  // half >= 0: a split block -- rows half*8..half*8+7 of the tile, each warp
-  // 16 rays (8x2) with lane l and l+16 marching the two halves of a ray.
-  int owned, half = -1;
+  // nseg > 1: a split block -- part `part` of the tile (16/nseg rows), each
+  // warp 32/nseg rays with lanes l, l+32/nseg, ... marching the nseg
+  // consecutive segments of one ray.  The first H4 tiles of the order are
+  // split in 4 (four blocks each), the next H2 in 2, the rest whole.
+  int owned, nseg = 1, part = 0;
   if (!BUDGET && kSplitRays && a.tile_order) {
     // capped by this launch's reserve: the order may come from a frame of
-    // another filter setting with a different split cap
-    const int H = min((int)a.tile_order[a.owned_tiles], a.split_max);
+    // another filter setting with another split cap
+    int H4 = (int)a.tile_order[a.owned_tiles];
+    int H2 = (int)a.tile_order[a.owned_tiles + 1];
+    if (3 * H4 > a.split_max) H4 = a.split_max / 3;
+    if (3 * H4 + H2 > a.split_max) H2 = a.split_max - 3 * H4;
     const int b = (int)blockIdx.x;
-    if (b < 2 * H) {
-      owned = (int)a.tile_order[b >> 1];
-      half = b & 1;
-    } else if (b - H < a.owned_tiles) {
-      owned = (int)a.tile_order[b - H];
+    if (b < 4 * H4) {
+      owned = (int)a.tile_order[b >> 2];
+      nseg = 4;
+      part = b & 3;
+    } else if (b < 4 * H4 + 2 * H2) {
+      owned = (int)a.tile_order[H4 + ((b - 4 * H4) >> 1)];
+      nseg = 2;
+      part = (b - 4 * H4) & 1;
+    } else if (b - 3 * H4 - H2 < a.owned_tiles) {
+      owned = (int)a.tile_order[b - 3 * H4 - H2];
     } else {
-      return;  // spare block (fewer than split_max tiles split), whole block
+      return;  // spare block (reserve not used up), whole block
     }
   } else {
     owned = a.tile_order ? (int)a.tile_order[blockIdx.x / kBlocksPerTile]
@@ -926,11 +936,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
 #endif
   const int tile = a.rank + a.world * owned;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-  const int seg = half >= 0 ? (int)((tid & 31) >> 4) : 0;
-  const int i = tx * kTileW + (half >= 0 ? (tid & 7) : (int)threadIdx.x);
-  const int j = half >= 0 ? ty * kTileH + half * 8 + 2 * (tid >> 5) + ((tid >> 3) & 1)
-                          : ty * kTileH + (int)(blockIdx.x % kBlocksPerTile) * (4 * kWarpsPerBlock) +
-                                (int)threadIdx.y;
+  const int rpw = 32 / nseg;  // rays per warp
+  const int seg = (int)(tid & 31) / rpw;
+  const int ray = (int)(tid & 31) % rpw;
+  const int i = tx * kTileW + (ray & 7);
+  const int j = nseg > 1 ? ty * kTileH + part * (kTileH / nseg) + (tid >> 5) * (rpw >> 3) + (ray >> 3)
+                         : ty * kTileH +
+                               (int)(blockIdx.x % kBlocksPerTile) * (4 * kWarpsPerBlock) +
+                               (int)threadIdx.y;
   bool valid = tile < a.n_tiles && i < a.C.W && j < a.C.H;
 
   bool hit = false;
@@ -968,38 +981,41 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
       limit = a.M.explicit_max > 0 ? a.M.explicit_max : own_budget(te, tx_, a.M.step);
     }
   }
-  // split ray: segment 0 marches samples [0, K) (it may run a little past K:
-  // its first hit is then still the ray's first hit), segment 1 marches
-  // [K, end) from the exact chunk base of sample K (the base recurrence
-  // applied K/chunk times); K chunk-aligned near the middle of the span
+  // split ray: segment s marches samples [s*K, (s+1)*K) (the last one to
+  // the end), starting from the exact chunk base of sample s*K (the base
+  // recurrence applied s*K/chunk times); K chunk-aligned.  A segment may run
+  // a little past its end: its first hit is then still the first hit after
+  // its start.  The ray's outcome is the first segment's hit, else the last
+  // segment's outcome.
   int K = 0, done0 = 0, stop = 0;
-  if (half >= 0 && live) {
+  if (nseg > 1 && live) {
     const float nsf = __fmul_rn(__fsub_rn(R.tend, R.base), a.M.inv_s);
-    K = nsf < 8.0f * a.M.chunk ? 0 : ((int)(0.5f * nsf) / a.M.chunk) * a.M.chunk;
+    K = nsf < 8.0f * a.M.chunk * nseg ? 0 : ((int)(nsf / nseg) / a.M.chunk) * a.M.chunk;
     if (K == 0) {
       live = seg == 0;  // too short to split: segment 0 marches it all
-    } else if (seg == 0) {
-      stop = K;
     } else {
-      for (int c = 0; c < K; c += a.M.chunk) R.base = __fadd_rn(R.base, a.M.adv);
-      done0 = K;
+      if (seg < nseg - 1) stop = (seg + 1) * K;
+      done0 = seg * K;
+      for (int c = 0; c < done0; c += a.M.chunk) R.base = __fadd_rn(R.base, a.M.adv);
     }
   }
   // all lanes of the warp march together (cooperative sample loads)
   {
     int st = march<KIND, CHECKED, DIAG, BUDGET>(a.V, a.M, a.F, lut, R, live, limit, done0, stop,
                                                 ht, hidx, nsamp, dg, &wsc[tid >> 5]);
-    if (half >= 0) {
-      // merge: segment 0's own hit wins, else segment 1's outcome
-      const int st1 = __shfl_down_sync(0xffffffffu, st, 16);
-      const float ht1 = __shfl_down_sync(0xffffffffu, ht, 16);
-      const int hidx1 = __shfl_down_sync(0xffffffffu, hidx, 16);
-      if (seg == 0 && K > 0 && st != kHit) {
-        st = st1;
-        ht = ht1;
-        hidx = hidx1;
+    if (nseg > 1) {
+      // merge pairwise toward segment 0: an earlier segment's hit wins
+      for (int o = rpw; o < 32; o <<= 1) {
+        const int st1 = __shfl_down_sync(0xffffffffu, st, o);
+        const float ht1 = __shfl_down_sync(0xffffffffu, ht, o);
+        const int hidx1 = __shfl_down_sync(0xffffffffu, hidx, o);
+        if ((seg & ((2 * o / rpw) - 1)) == 0 && K > 0 && st != kHit) {
+          st = st1;
+          ht = ht1;
+          hidx = hidx1;
+        }
       }
-      if (seg == 1) {
+      if (seg > 0) {
         st = kMiss;
         valid = false;
       }
@@ -1083,8 +1099,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
   if (a.tile_cost && lane == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    // ~microseconds; a split block stands for half of its tile's work
-    const unsigned long long us = ((t - block_t0) >> 10) << (half >= 0 ? 1 : 0);
+    // ~microseconds; a split block stands for 1/nseg of its tile's work
+    const unsigned long long us = ((t - block_t0) >> 10) * (unsigned)nseg;
     atomicMax(a.tile_cost + owned, (unsigned)min(us, 0xffffffffull));
   }
   if (a.O.image_hist) {
@@ -1118,11 +1134,12 @@ __global__ void span_max_kernel(const RayCamD C, int nx, int ny, int nz,
 
 // next frame's tile order from this frame's per-tile costs: heaviest first
 // (64 buckets, four per octave, descending; order within a bucket is
-// irrelevant, every order renders the same frame).  order[n] = H, the number
-// of leading tiles to split next frame: the tiles that would outlast the
+// irrelevant, every order renders the same frame).  order[n], order[n+1] =
+// H4, H2: the leading tiles to split next frame in 4 and in 2 segments: the
+// tiles that would outlast the
 // frame's ideal length (total cost / concurrent tile slots), when the
-// heaviest took >= split_us (split_us == 0: split every tile, tests).  One
-// block; resets the costs.
+// heaviest took >= split_us (split_us == 0: tests, see below).  One block;
+// resets the costs.
 __device__ __forceinline__ int cost_bucket(unsigned c) {
   if (c < 4) return (int)c;
   const int e = 31 - __clz(c);
@@ -1132,7 +1149,7 @@ __device__ __forceinline__ int cost_bucket(unsigned c) {
 
 __global__ void __launch_bounds__(1024) tile_order_kernel(uint32_t* __restrict__ cost,
                                                           uint32_t* __restrict__ order, int n,
-                                                          int split_max, int split_us, int slots) {
+                                                          int split_us, int slots) {
   __shared__ unsigned cnt[64];
   __shared__ unsigned long long total;
   __shared__ unsigned top;
@@ -1161,14 +1178,22 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(uint32_t* __restrict__
   }
   __syncthreads();
   if (tid == 0) {
-    unsigned heavy = 0;
-    if (split_us == 0) {
-      heavy = (unsigned)n;
+    // H4: tiles >= 2x the ideal length (split in 4), H2: tiles >= the ideal
+    // (split in 2); extra blocks 3*H4 + H2 within the launch's reserve
+    unsigned h4 = 0, h2 = 0;
+    if (split_us == 0) {  // tests: a quarter of the tiles in 4, a quarter in 2
+      h4 = (unsigned)n / 4;
+      h2 = (unsigned)n / 4;
     } else if (top >= (unsigned)split_us) {
-      const int bi = cost_bucket((unsigned)(total / (unsigned long long)(slots > 0 ? slots : 1)));
-      for (int b = 63; b >= bi; --b) heavy += cnt[b];
+      const unsigned long long ideal = total / (unsigned long long)(slots > 0 ? slots : 1);
+      const int b2 = cost_bucket((unsigned)min(ideal, 0xffffffffull));
+      const int b4 = cost_bucket((unsigned)min(2 * ideal, 0xffffffffull));
+      for (int b = 63; b >= b2; --b) (b >= b4 ? h4 : h2) += cnt[b];
     }
-    order[n] = heavy < (unsigned)split_max ? heavy : (unsigned)split_max;
+    // uncapped demand: the launch caps it to its reserve, and the host sizes
+    // the next reserve from it
+    order[n] = h4;
+    order[n + 1] = h2;
     unsigned run = 0;
     for (int b = 63; b >= 0; --b) {
       const unsigned c = cnt[b];
@@ -1642,7 +1667,8 @@ struct TileSched {
   const void* vol = nullptr;
   int w = 0, h = 0, rank = 0, world = 0, grid = 0;
   cudaStream_t stream = nullptr;
-  uint32_t* buf = nullptr;  // order[grid], H, then cost[grid]
+  uint32_t* buf = nullptr;  // order[grid], H4, H2, then cost[grid]
+  uint32_t* demand = nullptr;  // pinned host copy of H4, H2
   bool valid = false;
 };
 static thread_local TileSched tl_sched;
@@ -1651,7 +1677,7 @@ static thread_local TileSched tl_sched;
 // -1 = 4 waves of SMs) that gets an order, split threshold (us), split cap
 // (tiles = grid / div)
 static std::atomic<int> g_sched_order{-1}, g_sched_min_grid{-1}, g_sched_split_us{16},
-    g_sched_split_div{8};
+    g_sched_split_div{4};
 
 extern "C" int vx_set_schedule(int32_t tile_order, int32_t min_grid_tiles, int32_t split_min_us,
                                int32_t split_max_div) {
@@ -1686,8 +1712,10 @@ static int tile_sched(vx_volume* vol, const vx_ray_setup* rs, int rank, int worl
       VX_CUDA(cudaFree(t.buf));
       t.buf = nullptr;
     }
-    VX_CUDA(cudaMalloc(&t.buf, (size_t)grid * 8 + 4));
-    VX_CUDA(cudaMemsetAsync(t.buf + grid + 1, 0, (size_t)grid * 4, s));
+    VX_CUDA(cudaMalloc(&t.buf, (size_t)grid * 8 + 8));
+    if (!t.demand) VX_CUDA(cudaHostAlloc(&t.demand, 8, cudaHostAllocDefault));
+    t.demand[0] = t.demand[1] = 0;
+    VX_CUDA(cudaMemsetAsync(t.buf + grid + 2, 0, (size_t)grid * 4, s));
     t.vol = vol;
     t.w = rs->width;
     t.h = rs->height;
@@ -1761,13 +1789,20 @@ static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_p
   // ray splitting pays where heavy tiles are bound by the dependent lookup
   // chain; the entropy filter's heavy tiles are bound by filter evaluations
   // of rejected candidates, which a second segment only multiplies
-  // (C3 entropy 0.245 -> 0.345 ms measured), so it is not split
+  // (C3 entropy 0.245 -> 0.345 ms measured), so it is not split.  The
+  // reserve of extra blocks follows the last known demand (spare blocks
+  // still cost a launch slot each).
   a.split_max = a.F.kind == VX_FILTER_ENTROPY && g_sched_split_us.load() != 0
                     ? 0
                     : grid / g_sched_split_div.load();
   if (ts) {
-    a.tile_cost = ts->buf + grid + 1;
+    a.tile_cost = ts->buf + grid + 2;
     a.tile_order = ts->valid ? ts->buf : nullptr;
+    if (ts->valid) {
+      const long long want = 3ll * ts->demand[0] + ts->demand[1];
+      const long long reserve = want + want / 4 + 32;
+      if (reserve < a.split_max) a.split_max = (int)reserve;
+    }
   }
   if (checked)
     dispatch_raycast<true>(a, grid, s);
@@ -1775,10 +1810,13 @@ static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_p
     dispatch_raycast<false>(a, grid, s);
   VX_CHECK_LAUNCH();
   if (ts) {
-    tile_order_kernel<<<1, 1024, 0, s>>>(ts->buf + grid + 1, ts->buf, grid, a.split_max,
+    tile_order_kernel<<<1, 1024, 0, s>>>(ts->buf + grid + 2, ts->buf, grid,
                                          g_sched_split_us.load(),
                                          vx_sm_count() * (VX_RAYCAST_MIN_WARPS / kWarpsPerBlock));
     VX_CHECK_LAUNCH();
+    // the split demand, read back without a sync: it sizes a later frame's
+    // reserve of extra blocks (a stale value only costs time)
+    VX_CUDA(cudaMemcpyAsync(ts->demand, ts->buf + grid, 8, cudaMemcpyDeviceToHost, s));
     ts->valid = true;
   }
   return VX_OK;

@@ -332,7 +332,7 @@ def split_everything():
 
     _lib.call("vx_set_schedule", 1, 0, 0, 1)
     yield
-    _lib.call("vx_set_schedule", -1, -1, 16, 8)
+    _lib.call("vx_set_schedule", -1, -1, 16, 4)
 
 
 def test_split_rays_and_tile_order_match_oracle(vx, oracle, split_everything):
