@@ -173,6 +173,12 @@ int vx_histogram_device(const uint8_t* dev, uint64_t n, uint64_t* dev_counts, vo
 int vx_otsu(const uint64_t counts[256], int32_t* T_out);
 /* K2 on device counts; writes the threshold to dev_T (int32) */
 int vx_otsu_device(const uint64_t* dev_counts, int32_t* dev_T, void* stream);
+/* K1+K2 in ONE launch over n device bytes: dev_counts[256] is overwritten with
+ * the counts (np.bincount, histogram.py:120) and dev_T receives the exact Otsu
+ * threshold (histogram.py:59-101), or -1 when n == 0 or n >= 2^47.  The last
+ * block to finish runs the Otsu scan.  Asynchronous on `stream`. */
+int vx_histogram_otsu_device(const uint8_t* dev, uint64_t n, uint64_t* dev_counts,
+                             int32_t* dev_T, void* stream);
 /* K6: image entropy of n grey pixels (metrics.py:26-33); also returns counts */
 int vx_image_entropy(const uint8_t* host_pixels, int64_t n, double* H_out,
                      uint64_t counts_out[256]);

@@ -125,6 +125,7 @@ SIGNATURES = {
     "vx_histogram_device": [P, U64, P, P],
     "vx_otsu": [P, P],
     "vx_otsu_device": [P, P, P],
+    "vx_histogram_otsu_device": [P, U64, P, P, P],
     "vx_image_entropy": [P, I64, P, P],
     "vx_entropy_from_counts_device": [P, U64, P, P],
     "vx_render": [P, P, P, P, P, P],

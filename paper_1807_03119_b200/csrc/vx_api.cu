@@ -191,10 +191,10 @@ int vx_volume_alloc(int64_t nx, int64_t ny, int64_t nz, vx_volume** out) {
 // compact device bytes -> padded layout + histogram + brick map
 int vx_volume_finish(vx_volume* v, const uint8_t* compact_dev, cudaStream_t s) {
   uint64_t* dcounts = nullptr;
-  VX_CUDA(vx_malloc_async(&dcounts, 256 * 8, s));
-  VX_CUDA(cudaMemsetAsync(dcounts, 0, 256 * 8, s));
+  VX_CUDA(vx_malloc_async(&dcounts, 257 * 8, s));
   const uint64_t n = (uint64_t)v->nx * v->ny * v->nz;
-  int rc = vx_launch_hist(compact_dev, n, dcounts, s);
+  // K1 (+ the fused K2 scan, whose T is recomputed by otsu() on demand)
+  int rc = vx_launch_hist_otsu(compact_dev, n, dcounts, reinterpret_cast<int32_t*>(dcounts + 256), s);
   if (rc) return rc;
   VX_CUDA(cudaMemsetAsync(v->alloc, 0, v->alloc_bytes, s));
   cudaMemcpy3DParms p;
@@ -503,6 +503,15 @@ extern "C" int vx_otsu_device(const uint64_t* dev_counts, int32_t* dev_T, void* 
   }
   cudaStream_t s = (cudaStream_t)stream;
   return vx_launch_otsu(dev_counts, dev_T, s);
+}
+
+extern "C" int vx_histogram_otsu_device(const uint8_t* dev, uint64_t n, uint64_t* dev_counts,
+                                        int32_t* dev_T, void* stream) {
+  if ((!dev && n) || !dev_counts || !dev_T) {
+    vx_set_error("vx_histogram_otsu_device: null argument");
+    return VX_EINVAL;
+  }
+  return vx_launch_hist_otsu(dev, n, dev_counts, dev_T, (cudaStream_t)stream);
 }
 
 extern "C" int vx_otsu(const uint64_t counts[256], int32_t* T_out) {

@@ -7,6 +7,18 @@
 
 namespace {
 
+#ifdef VX_HIST_TIMING
+__device__ unsigned long long g_ht[8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define VX_HT(k) do { if (threadIdx.x == 0 && gridDim.x > 1) { asm volatile("" ::: "memory"); g_ht[k] = gtimer(); } } while (0)
+#else
+#define VX_HT(k) do {} while (0)
+#endif
+
 constexpr int kHistThreads = 512;
 constexpr int kHistBlocksPerSM = 4;
 
@@ -29,9 +41,10 @@ __device__ __forceinline__ void count_word(uint32_t* lane_base, uint32_t w) {
   atomicAdd(lane_base + ((w >> 24) << 5), 1u);
 }
 
-__global__ void __launch_bounds__(kHistThreads)
-hist256_kernel(const uint8_t* __restrict__ data, uint64_t n, unsigned long long* __restrict__ out) {
-  __shared__ uint32_t sh[256 * 32];
+// Counts this block's share of data[0, n) into the [bin][lane] shared table
+// `sh` (zeroed here) and reduces it to per-bin block totals tot[256].
+__device__ __forceinline__ void hist_block_local(const uint8_t* __restrict__ data, uint64_t n,
+                                                 uint32_t* sh, uint32_t* tot) {
   for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) sh[i] = 0u;
   __syncthreads();
 
@@ -68,10 +81,22 @@ hist256_kernel(const uint8_t* __restrict__ data, uint64_t n, unsigned long long*
     count_word(lane_base, d.x); count_word(lane_base, d.y);
     count_word(lane_base, d.z); count_word(lane_base, d.w);
   }
-  for (; i < nvec; i += nthreads) {
-    uint4 a = ld_stream(vec + i);
-    count_word(lane_base, a.x); count_word(lane_base, a.y);
-    count_word(lane_base, a.z); count_word(lane_base, a.w);
+  // remainder (< 4 vectors per thread): loads issued together, so a thread
+  // waits on one memory round trip instead of up to three in a row
+  if (i < nvec) {
+    uint4 v[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const uint64_t j = i + k * nthreads;
+      v[k] = j < nvec ? ld_stream(vec + j) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (i + k * nthreads < nvec) {
+        count_word(lane_base, v[k].x); count_word(lane_base, v[k].y);
+        count_word(lane_base, v[k].z); count_word(lane_base, v[k].w);
+      }
+    }
   }
   __syncthreads();
 
@@ -80,8 +105,25 @@ hist256_kernel(const uint8_t* __restrict__ data, uint64_t n, unsigned long long*
     uint32_t s = 0;
 #pragma unroll 8
     for (int j = 0; j < 32; ++j) s += sh[b * 32 + ((j + b) & 31)];
-    if (s) atomicAdd(out + b, (unsigned long long)s);
+    tot[b] = s;
   }
+}
+
+// Block-local histogram, then the block's 256 totals into out[256] (u64
+// atomics; a DSMEM pre-merge across 2/4/8-block clusters measured no faster).
+__device__ __forceinline__ void hist_block(const uint8_t* __restrict__ data, uint64_t n,
+                                           uint32_t* sh, uint32_t* tot, unsigned long long* out) {
+  hist_block_local(data, n, sh, tot);
+  __syncthreads();
+  for (int b = threadIdx.x; b < 256; b += blockDim.x)
+    if (tot[b]) atomicAdd(out + b, (unsigned long long)tot[b]);
+}
+
+__global__ void __launch_bounds__(kHistThreads)
+hist256_kernel(const uint8_t* __restrict__ data, uint64_t n, unsigned long long* __restrict__ out) {
+  __shared__ __align__(16) uint32_t sh[256 * 32];
+  __shared__ uint32_t tot[256];
+  hist_block(data, n, sh, tot, out);
 }
 
 // ---------------------------------------------------------------------------
@@ -176,31 +218,28 @@ __device__ bool frac_less(const U192& numA, const U128& denA, const U192& numB, 
   return false;
 }
 
-__global__ void __launch_bounds__(256) otsu_kernel(const unsigned long long* __restrict__ counts,
-                                                   int32_t* __restrict__ T_out) {
-  __shared__ unsigned long long sn[256], sb[256], sa[256];
-  __shared__ U192 snum[256];
-  __shared__ U128 sden[256];
-  __shared__ int st[256];
-  const int t = threadIdx.x;
-  const unsigned long long c = counts[t];
-  sn[t] = c;
-  sb[t] = c * (unsigned long long)t;
-  sa[t] = c * (unsigned long long)(t * t);
-  __syncthreads();
-  // inclusive Hillis-Steele scans (u64 is exact: N < 2^47)
-  for (int off = 1; off < 256; off <<= 1) {
-    unsigned long long vn = 0, vb = 0, va = 0;
-    if (t >= off) { vn = sn[t - off]; vb = sb[t - off]; va = sa[t - off]; }
-    __syncthreads();
-    sn[t] += vn; sb[t] += vb; sa[t] += va;
-    __syncthreads();
-  }
-  const unsigned long long N = sn[255], B = sb[255], A = sa[255];
-  const unsigned long long n0 = sn[t], b0 = sb[t], a0 = sa[t];
+struct OtsuSmem {
+  unsigned long long sn[256], sb[256], sa[256];  // inclusive prefix sums
+  unsigned long long wt[8][3];                    // warp totals
+  double wmin[8];
+  unsigned wmask[8];
+};
+
+__device__ __forceinline__ unsigned long long shfl_up_u64(unsigned long long v, int d) {
+  return __shfl_up_sync(0xffffffffu, v, d);
+}
+
+__device__ __forceinline__ double u128_to_double(U128 x) {
+  return __dadd_rn(__dmul_rn(__ull2double_rn(x.w[1]), 18446744073709551616.0),
+                   __ull2double_rn(x.w[0]));
+}
+
+// Exact objective N*sigma_w^2(T) = num/den of histogram.py:92-97 from the
+// prefix sums (n0, b0, a0) and the totals; an empty class contributes 0.
+__device__ void otsu_exact(unsigned long long n0, unsigned long long b0, unsigned long long a0,
+                           unsigned long long N, unsigned long long B, unsigned long long A,
+                           U192& num, U128& den) {
   const unsigned long long n1 = N - n0, b1 = B - b0, a1 = A - a0;
-  U192 num;
-  U128 den;
   if (n0 && n1) {
     U128 x0 = sub_128(mul_64_64(a0, n0), mul_64_64(b0, b0));
     U128 x1 = sub_128(mul_64_64(a1, n1), mul_64_64(b1, b1));
@@ -215,20 +254,160 @@ __global__ void __launch_bounds__(256) otsu_kernel(const unsigned long long* __r
     num.w[0] = x1.w[0]; num.w[1] = x1.w[1]; num.w[2] = 0;
     den.w[0] = n1; den.w[1] = 0;
   }
-  snum[t] = num;
-  sden[t] = den;
-  st[t] = t;
-  __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
-    if (t < s) {
-      const int o = t + s;
-      bool take = frac_less(snum[o], sden[o], snum[t], sden[t]);
-      if (!take && !frac_less(snum[t], sden[t], snum[o], sden[o]) && st[o] < st[t]) take = true;
-      if (take) { snum[t] = snum[o]; sden[t] = sden[o]; st[t] = st[o]; }
+}
+
+// Exact Otsu of the 256 counts held by threads 0..255 (thread t holds bin t;
+// `c` is ignored for t >= 256).  Every thread of the block must call it.
+//
+// Screen, then decide exactly.  Each T gets an FP64 estimate f_d of its exact
+// objective f = num/den: x0 = a0*n0 - b0^2 and x1 are formed EXACTLY in
+// 128-bit integers (no cancellation in floating point), then
+// f_d = (n1*x0 + n0*x1) / (n0*n1) over positive terms only, so
+// |f_d - f| <= 8 * 2^-53 * f, and f_d = 0 exactly when f = 0.  Hence the exact
+// argmin T* satisfies f_d(T*) <= min_T f_d * (1 + 2^-30), and only T passing
+// that screen are compared exactly (320-bit cross products, histogram.py:98),
+// in increasing T with a strict compare (ties -> smallest T).  T with c[T] = 0
+// (T > 0) repeat the partition of T - 1, so they can never be the smallest
+// minimiser and are screened out; this keeps exact-tie plateaus of sparse
+// histograms to one candidate each.  Typically one candidate survives; the
+// former all-exact argmin tree took ~9 us of a single block.
+__device__ void otsu_block(unsigned long long c, OtsuSmem& S, int32_t* __restrict__ T_out) {
+  const int t = threadIdx.x;
+  const int lane = t & 31, w = t >> 5;
+  const bool on = t < 256;
+  unsigned long long n = 0, b = 0, a = 0;
+  if (on) {
+    // warp-inclusive scans of n, sum i*c, sum i^2*c (u64 is exact: N < 2^47)
+    n = c;
+    b = c * (unsigned long long)t;
+    a = c * (unsigned long long)(t * t);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned long long vn = shfl_up_u64(n, d), vb = shfl_up_u64(b, d),
+                               va = shfl_up_u64(a, d);
+      if (lane >= d) { n += vn; b += vb; a += va; }
     }
-    __syncthreads();
+    if (lane == 31) { S.wt[w][0] = n; S.wt[w][1] = b; S.wt[w][2] = a; }
   }
-  if (t == 0) *T_out = (N == 0 || N >= (1ull << 47)) ? -1 : st[0];
+  VX_HT(6);
+  __syncthreads();
+  VX_HT(0);
+  unsigned long long N = 0, B = 0, A = 0;
+  for (int k = 0; k < 8; ++k) {
+    if (k < w) { n += S.wt[k][0]; b += S.wt[k][1]; a += S.wt[k][2]; }
+    N += S.wt[k][0]; B += S.wt[k][1]; A += S.wt[k][2];
+  }
+  const bool valid = N != 0 && N < (1ull << 47);
+  double f = __longlong_as_double(0x7ff0000000000000ll);  // +inf: not a candidate
+  if (on) {
+    S.sn[t] = n; S.sb[t] = b; S.sa[t] = a;
+    if (valid && (t == 0 || c != 0)) {
+      const unsigned long long n1 = N - n, b1 = B - b, a1 = A - a;
+      if (n && n1) {
+        const double x0 = u128_to_double(sub_128(mul_64_64(a, n), mul_64_64(b, b)));
+        const double x1 = u128_to_double(sub_128(mul_64_64(a1, n1), mul_64_64(b1, b1)));
+        const double dn0 = (double)n, dn1 = (double)n1;
+        f = __ddiv_rn(__dadd_rn(__dmul_rn(dn1, x0), __dmul_rn(dn0, x1)), __dmul_rn(dn0, dn1));
+      } else if (n) {
+        f = __ddiv_rn(u128_to_double(sub_128(mul_64_64(a, n), mul_64_64(b, b))), (double)n);
+      } else {
+        f = __ddiv_rn(u128_to_double(sub_128(mul_64_64(a1, n1), mul_64_64(b1, b1))), (double)n1);
+      }
+    }
+    double m = f;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, d));
+    if (lane == 0) S.wmin[w] = m;
+  }
+  __syncthreads();
+  VX_HT(1);
+  if (on) {
+    double m = S.wmin[0];
+    for (int k = 1; k < 8; ++k) m = fmin(m, S.wmin[k]);
+    const double cut = __dmul_ru(m, 1.0 + 0x1p-30);
+    const unsigned mask = __ballot_sync(0xffffffffu, f <= cut);
+    if (lane == 0) S.wmask[w] = mask;
+  }
+  __syncthreads();
+  VX_HT(2);
+  if (t != 0) return;
+  if (!valid) {
+    *T_out = -1;
+    return;
+  }
+  int best = -1;
+  U192 bnum;
+  U128 bden;
+  for (int k = 0; k < 8; ++k) {
+    unsigned mk = S.wmask[k];
+    while (mk) {
+      const int T = k * 32 + __ffs(mk) - 1;
+      mk &= mk - 1;
+      U192 num;
+      U128 den;
+      otsu_exact(S.sn[T], S.sb[T], S.sa[T], N, B, A, num, den);
+      if (best < 0 || frac_less(num, den, bnum, bden)) {
+        best = T;
+        bnum = num;
+        bden = den;
+      }
+    }
+  }
+  *T_out = best;
+  VX_HT(3);
+}
+
+__global__ void __launch_bounds__(256) otsu_kernel(const unsigned long long* __restrict__ counts,
+                                                   int32_t* __restrict__ T_out) {
+  __shared__ OtsuSmem S;
+  otsu_block(counts[threadIdx.x], S, T_out);
+}
+
+// K1+K2 in one launch (histogram.py:119-133 then :59-101).  Blocks add their
+// bins into the workspace ws[0..255]; the last block to finish (ticket in
+// ws[256]) copies them to counts_out, re-zeroes the workspace for the next
+// call on this stream, and runs the exact Otsu scan over the shared memory
+// its histogram used.  One launch, no memset: the stand-alone K1 + K2 pair
+// costs two launch gaps and a fill kernel, which is 10-20 us at 256^3-512^3.
+struct HistWs {
+  unsigned long long bins[256];
+  unsigned int ticket;
+};
+
+__global__ void __launch_bounds__(kHistThreads, kHistBlocksPerSM)
+hist_otsu_kernel(const uint8_t* __restrict__ data, uint64_t n, HistWs* __restrict__ ws,
+                 unsigned long long* __restrict__ counts_out, int32_t* __restrict__ T_out) {
+  static_assert(sizeof(OtsuSmem) <= 256 * 32 * 4, "Otsu scratch must fit the histogram table");
+  __shared__ __align__(16) uint32_t sh[256 * 32];
+  __shared__ uint32_t tot[256];
+  __shared__ bool last;
+  hist_block(data, n, sh, tot, ws->bins);
+  // the block's bin atomics precede thread 0's fence (barrier), which
+  // precedes its ticket; one fencing thread per block, as in the CUDA
+  // guide's last-block reduction.  The last block's tail (bins, scan,
+  // screen, exact compare) measures ~7 us with %globaltimer marks
+  // (-DVX_HIST_TIMING, scripts/hist_tail_times.py), most of it straight-line
+  // code that no block has executed before (cold instruction fetch).
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&ws->ticket, 1u) == gridDim.x - 1;
+    if (last) __threadfence();
+  }
+  __syncthreads();
+  if (!last) return;
+  VX_HT(7);
+  unsigned long long c = 0;
+  if (threadIdx.x < 256) c = __ldcg(ws->bins + threadIdx.x);
+  VX_HT(4);
+  otsu_block(c, *reinterpret_cast<OtsuSmem*>(sh), T_out);
+  VX_HT(5);
+  // outputs and the workspace reset leave after the scan (off its path)
+  if (threadIdx.x < 256) {
+    counts_out[threadIdx.x] = c;
+    ws->bins[threadIdx.x] = 0ull;
+  }
+  if (threadIdx.x == 0) ws->ticket = 0u;
 }
 
 // ---------------------------------------------------------------------------
@@ -297,6 +476,53 @@ int vx_launch_hist(const uint8_t* dev, uint64_t n, uint64_t* dev_counts, cudaStr
   VX_CHECK_LAUNCH();
   return VX_OK;
 }
+
+// one zeroed workspace per (device, stream): the kernel's last block leaves
+// it zeroed, and launches on one stream are ordered
+static std::mutex g_ws_mu;
+static struct WsSlot { int dev; cudaStream_t s; HistWs* p; } g_ws[64];
+static int g_ws_n = 0;
+
+static int hist_ws(cudaStream_t s, HistWs** out) {
+  int dev = 0;
+  VX_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  for (int i = 0; i < g_ws_n; ++i)
+    if (g_ws[i].dev == dev && g_ws[i].s == s) {
+      *out = g_ws[i].p;
+      return VX_OK;
+    }
+  HistWs* p = nullptr;
+  VX_CUDA(cudaMalloc(&p, sizeof(HistWs)));
+  VX_CUDA(cudaMemset(p, 0, sizeof(HistWs)));
+  const int slot = g_ws_n < 64 ? g_ws_n++ : (int)(((uintptr_t)s >> 4) % 64);
+  // a recycled slot's old workspace stays allocated: a launch may still use it
+  g_ws[slot] = {dev, s, p};
+  *out = p;
+  return VX_OK;
+}
+
+int vx_launch_hist_otsu(const uint8_t* dev, uint64_t n, uint64_t* dev_counts, int32_t* dev_T,
+                        cudaStream_t s) {
+  HistWs* ws = nullptr;
+  int rc = hist_ws(s, &ws);
+  if (rc) return rc;
+  const int sms = vx_sm_count();
+  uint64_t want = (n / 16 + kHistThreads - 1) / kHistThreads;
+  uint64_t grid = (uint64_t)sms * kHistBlocksPerSM;
+  if (want < grid) grid = want ? want : 1;
+  hist_otsu_kernel<<<(unsigned)grid, kHistThreads, 0, s>>>(
+      dev, n, ws, reinterpret_cast<unsigned long long*>(dev_counts), dev_T);
+  VX_CHECK_LAUNCH();
+  return VX_OK;
+}
+
+#ifdef VX_HIST_TIMING
+extern "C" int vx_debug_hist_times(unsigned long long* out) {
+  VX_CUDA(cudaMemcpyFromSymbol(out, g_ht, 8 * 8));
+  return VX_OK;
+}
+#endif
 
 int vx_launch_otsu(const uint64_t* dev_counts, int32_t* dev_T, cudaStream_t s) {
   otsu_kernel<<<1, 256, 0, s>>>(reinterpret_cast<const unsigned long long*>(dev_counts), dev_T);

@@ -108,6 +108,9 @@ int vx_get_dist_map(vx_volume* v, int thr, const uint8_t** map_out, cudaStream_t
 // launchers implemented across translation units
 int vx_launch_hist(const uint8_t* dev, uint64_t n, uint64_t* dev_counts, cudaStream_t s);
 int vx_launch_otsu(const uint64_t* dev_counts, int32_t* dev_T, cudaStream_t s);
+// K1+K2 fused: dev_counts[256] overwritten, dev_T = Otsu T (-1: empty / >= 2^47)
+int vx_launch_hist_otsu(const uint8_t* dev, uint64_t n, uint64_t* dev_counts, int32_t* dev_T,
+                        cudaStream_t s);
 int vx_launch_entropy(const uint64_t* dev_counts, uint64_t n, double* dev_H, cudaStream_t s);
 int vx_launch_brick_max(vx_volume* v, cudaStream_t s);
 int vx_launch_dist_map(const vx_volume* v, int thr, uint8_t* map, cudaStream_t s);

@@ -78,6 +78,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--skip-4096", action="store_true")
     ap.add_argument("--frames-only", action="store_true", help="skip the C5 histogram sweep")
+    ap.add_argument("--hist-only", action="store_true", help="only the C5 histogram sweep")
     args = ap.parse_args()
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -99,10 +100,12 @@ def main():
                      "filters": rows}
         dvol.free()
 
-    frames("C1_spot64_256", phantoms.spot_phantom_spec(64), 256, KINDS)
-    frames("C2_C3_insect512_1024", phantoms.insect_phantom_spec(512), 1024, KINDS)
-    frames("bench_insect1024_1024", phantoms.insect_phantom_spec(1024), 1024, ("local-cluster",))
-    frames("C4_insect2048_2048", phantoms.insect_phantom_spec(2048), 2048, ("local-cluster",))
+    if not args.hist_only:
+        frames("C1_spot64_256", phantoms.spot_phantom_spec(64), 256, KINDS)
+        frames("C2_C3_insect512_1024", phantoms.insect_phantom_spec(512), 1024, KINDS)
+        frames("bench_insect1024_1024", phantoms.insect_phantom_spec(1024), 1024,
+               ("local-cluster",))
+        frames("C4_insect2048_2048", phantoms.insect_phantom_spec(2048), 2048, ("local-cluster",))
 
     peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists(
         "MEASURED_PEAKS.json") else 6650.0
@@ -128,10 +131,8 @@ def main():
         sp = C.c_void_p(stream.cuda_stream)
 
         def run():
-            counts.zero_()
-            _lib.call("vx_histogram_device", C.c_void_p(t.data_ptr()), n,
-                      C.c_void_p(counts.data_ptr()), sp)
-            _lib.call("vx_otsu_device", C.c_void_p(counts.data_ptr()), C.c_void_p(dT.data_ptr()), sp)
+            _lib.call("vx_histogram_otsu_device", C.c_void_p(t.data_ptr()), n,
+                      C.c_void_p(counts.data_ptr()), C.c_void_p(dT.data_ptr()), sp)
 
         ms = timed(run, args.reps, flush)
         gbs = n / (ms * 1e-3) / 1e9

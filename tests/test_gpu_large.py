@@ -55,6 +55,15 @@ def test_c5_histogram_sweep_exact(edge):
     from paper_1807_03119_b200.histogram import otsu
 
     assert otsu(counts) == orc.otsu(counts) == 127  # flat histogram splits in the middle
+    # one-launch K1+K2 over the whole volume
+    fc = torch.full((256,), -1, dtype=torch.int64, device="cuda")
+    fT = torch.zeros(1, dtype=torch.int32, device="cuda")
+    from paper_1807_03119_b200 import _lib
+
+    _lib.call("vx_histogram_otsu_device", C.c_void_p(t.data_ptr()), n, C.c_void_p(fc.data_ptr()),
+              C.c_void_p(fT.data_ptr()), C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    assert np.array_equal(fc.cpu().numpy(), counts) and int(fT.item()) == 127
     del t
 
 

@@ -28,6 +28,69 @@ def test_k1_histogram_sizes(vx, oracle, n):
     assert np.array_equal(histogram_of_bytes(data), oracle.hist256(data))
 
 
+def _fused(t, n, stream=None):
+    """vx_histogram_otsu_device (K1+K2 in one launch) over device bytes."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1807_03119_b200 import _lib
+
+    s = stream or torch.cuda.current_stream()
+    counts = torch.full((256,), -1, dtype=torch.int64, device="cuda")
+    T = torch.full((1,), -7, dtype=torch.int32, device="cuda")
+    _lib.call("vx_histogram_otsu_device", C.c_void_p(t.data_ptr() if n else 0), n,
+              C.c_void_p(counts.data_ptr()), C.c_void_p(T.data_ptr()), C.c_void_p(s.cuda_stream))
+    return counts, T
+
+
+@pytest.mark.parametrize("n", [0, 1, 7, 16, 17, 4096 + 3, 1 << 20, (1 << 24) + 11, (1 << 27) + 5])
+def test_fused_hist_otsu_sizes(vx, oracle, n):
+    """One-launch K1+K2: counts bit-exact, T equal to the exact oracle Otsu;
+    back-to-back calls on one stream (the workspace resets itself) and on a
+    second stream agree."""
+    import torch
+
+    rs = np.random.default_rng(n + 3)
+    host = rs.integers(0, 256, n, dtype=np.uint8)
+    host[: n // 2] = rs.integers(0, 30, n // 2, dtype=np.uint8)  # bimodal-ish
+    t = torch.from_numpy(host).cuda()
+    want = oracle.hist256(host)
+    want_T = oracle.otsu(want) if n else -1
+    side = torch.cuda.Stream()
+    for rep in range(3):
+        for s in (None, side):
+            off = 3 if (rep == 2 and n > 3) else 0  # unaligned start
+            sub = t[off:]
+            counts, T = _fused(sub, n - off, s)
+            torch.cuda.synchronize()
+            w = want if off == 0 else oracle.hist256(host[off:])
+            assert np.array_equal(counts.cpu().numpy(), w)
+            wt = want_T if off == 0 else (oracle.otsu(w) if n - off else -1)
+            assert int(T.item()) == wt
+
+
+def test_fused_hist_otsu_goldens(vx, oracle):
+    """The reference's golden Otsu histograms, expanded to bytes where small."""
+    import torch
+
+    g = golden("otsu.npz")
+    done = 0
+    for counts, thr in zip(g["counts"], g["threshold"]):
+        if int(np.sum(counts)) > (1 << 22):
+            continue
+        host = np.repeat(np.arange(256, dtype=np.uint8), np.asarray(counts, dtype=np.int64))
+        np.random.default_rng(done).shuffle(host)
+        c, T = _fused(torch.from_numpy(host).cuda(), host.size)
+        torch.cuda.synchronize()
+        assert np.array_equal(c.cpu().numpy(), counts)
+        assert int(T.item()) == thr
+        done += 1
+        if done == 200:
+            break
+    assert done >= 50
+
+
 def test_k1_unaligned_and_skewed(vx, oracle):
     from paper_1807_03119_b200.histogram import histogram_of_bytes
 
