@@ -195,8 +195,16 @@ def check(rc: int, exc_type=None):
     raise NativeError(rc, msg)
 
 
+_fns: dict = {}
+
+
 def call(name: str, *args, exc_type=None):
-    check(getattr(load(), name)(*args), exc_type)
+    fn = _fns.get(name)
+    if fn is None:
+        fn = _fns[name] = getattr(load(), name)
+    rc = fn(*args)
+    if rc != VX_OK:
+        check(rc, exc_type)
 
 
 _device_ok = None
@@ -250,9 +258,14 @@ class PinnedPool:
             lst = self._free.get(nbytes)
             ptr = lst.pop() if lst else None
         if ptr is None:
-            p = C.c_void_p()
+            # a miss allocates a spare too: a caller that keeps the previous
+            # frame while rendering the next (double buffering) then never
+            # pays cudaHostAlloc (~3-5 ms per MiB) inside its loop
+            p, spare = C.c_void_p(), C.c_void_p()
             call("vx_host_alloc", nbytes, C.byref(p))
+            call("vx_host_alloc", nbytes, C.byref(spare))
             ptr = p.value
+            self._release(nbytes, spare.value)
         buf = (C.c_uint8 * max(nbytes, 1)).from_address(ptr)
         weakref.finalize(buf, self._release, nbytes, ptr)
         return np.frombuffer(buf, dtype=dtype, count=count).reshape(shape), ptr

@@ -1729,9 +1729,30 @@ static int tile_sched(vx_volume* vol, const vx_ray_setup* rs, int rank, int worl
   return VX_OK;
 }
 
+// the next frame's tile order (tile_order_kernel + the split-demand read
+// back); it only has to precede the next frame on this stream
+struct OrderJob {
+  TileSched* ts = nullptr;
+  int grid = 0;
+};
+
+static int order_tiles(const OrderJob& j, cudaStream_t s) {
+  if (!j.ts) return VX_OK;
+  TileSched* ts = j.ts;
+  tile_order_kernel<<<1, 1024, 0, s>>>(ts->buf + j.grid + 2, ts->buf, j.grid,
+                                       g_sched_split_us.load(),
+                                       vx_sm_count() * (VX_RAYCAST_MIN_WARPS / kWarpsPerBlock));
+  VX_CHECK_LAUNCH();
+  // the split demand, read back without a sync: it sizes a later frame's
+  // reserve of extra blocks (a stale value only costs time)
+  VX_CUDA(cudaMemcpyAsync(ts->demand, ts->buf + j.grid, 8, cudaMemcpyDeviceToHost, s));
+  ts->valid = true;
+  return VX_OK;
+}
+
 static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_params* rp,
                        const vx_filter_config* fc, const vx_partition* part, vx_render_out* o,
-                       cudaStream_t s, int explicit_budget_override) {
+                       cudaStream_t s, int explicit_budget_override, OrderJob* defer = nullptr) {
   if (!vol || !rs || !rp || !fc || !o || !o->pixels) {
     vx_set_error("vx_render: null argument");
     return VX_EINVAL;
@@ -1809,17 +1830,14 @@ static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_p
   else
     dispatch_raycast<false>(a, grid, s);
   VX_CHECK_LAUNCH();
-  if (ts) {
-    tile_order_kernel<<<1, 1024, 0, s>>>(ts->buf + grid + 2, ts->buf, grid,
-                                         g_sched_split_us.load(),
-                                         vx_sm_count() * (VX_RAYCAST_MIN_WARPS / kWarpsPerBlock));
-    VX_CHECK_LAUNCH();
-    // the split demand, read back without a sync: it sizes a later frame's
-    // reserve of extra blocks (a stale value only costs time)
-    VX_CUDA(cudaMemcpyAsync(ts->demand, ts->buf + grid, 8, cudaMemcpyDeviceToHost, s));
-    ts->valid = true;
+  OrderJob job;
+  job.ts = ts;
+  job.grid = grid;
+  if (defer) {
+    *defer = job;
+    return VX_OK;
   }
-  return VX_OK;
+  return order_tiles(job, s);
 }
 
 // exact frame budget of render.py:469-473
@@ -1871,6 +1889,22 @@ extern "C" int vx_last_render_ms(float* ms_out) {
   }
   *ms_out = tl_render_ms;
   return VX_OK;
+}
+
+static thread_local cudaEvent_t tl_copy_ev = nullptr;
+static thread_local int tl_copy_dev = -1;
+
+static cudaError_t copy_event(cudaEvent_t* ev) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (!tl_copy_ev || tl_copy_dev != dev) {
+    e = cudaEventCreateWithFlags(&tl_copy_ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+    tl_copy_dev = dev;
+  }
+  *ev = tl_copy_ev;
+  return cudaSuccess;
 }
 
 static int timing_events(cudaEvent_t** ev) {
@@ -1935,16 +1969,21 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
     if (rc) return rc;
     VX_CUDA(cudaEventRecord(ev[0], s));
   }
-  rc = render_impl(vol, rs, rp, fc, part, &d, s, 0);
+  OrderJob order;
+  rc = render_impl(vol, rs, rp, fc, part, &d, s, 0, &order);
   if (rc) return rc;
   if (timed) VX_CUDA(cudaEventRecord(ev[1], s));
   float ms = 0.0f;
   // one synchronisation: counters and every requested output come back
-  // together; the rare truncation re-render (below) copies again
+  // together; the rare truncation re-render (below) copies again.  The copies
+  // are queued right behind K4; the next frame's tile ordering goes behind
+  // them and the host waits only for the copies (event), not for it.
   uint64_t small_h[267];
+  cudaEvent_t copied = nullptr;
+  VX_CUDA(copy_event(&copied));
   auto copy_back = [&]() -> int {
-    VX_CUDA(cudaMemcpyAsync(small_h, small, sizeof(small_h), cudaMemcpyDeviceToHost, s));
     VX_CUDA(cudaMemcpyAsync(out->pixels, d.pixels, npx, cudaMemcpyDeviceToHost, s));
+    VX_CUDA(cudaMemcpyAsync(small_h, small, sizeof(small_h), cudaMemcpyDeviceToHost, s));
     if (out->hit_voxel)
       VX_CUDA(cudaMemcpyAsync(out->hit_voxel, d.hit_voxel, npx * 12, cudaMemcpyDeviceToHost, s));
     if (out->hit_t) VX_CUDA(cudaMemcpyAsync(out->hit_t, d.hit_t, npx * 4, cudaMemcpyDeviceToHost, s));
@@ -1952,7 +1991,11 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
       VX_CUDA(cudaMemcpyAsync(out->hit_value, d.hit_value, npx * 8, cudaMemcpyDeviceToHost, s));
     if (out->intensity)
       VX_CUDA(cudaMemcpyAsync(out->intensity, d.intensity, npx * 8, cudaMemcpyDeviceToHost, s));
-    VX_CUDA(cudaStreamSynchronize(s));
+    VX_CUDA(cudaEventRecord(copied, s));
+    int r2 = order_tiles(order, s);
+    order = OrderJob();
+    if (r2) return r2;
+    VX_CUDA(cudaEventSynchronize(copied));
     return VX_OK;
   };
   rc = copy_back();
@@ -1967,7 +2010,7 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
     if (rc) return rc;
     VX_CUDA(cudaMemsetAsync(small, 0, 267 * 8, s));
     if (timed) VX_CUDA(cudaEventRecord(ev[0], s));
-    rc = render_impl(vol, rs, rp, fc, part, &d, s, budget);
+    rc = render_impl(vol, rs, rp, fc, part, &d, s, budget, &order);
     if (rc) return rc;
     if (timed) VX_CUDA(cudaEventRecord(ev[1], s));
     rc = copy_back();

@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import threading
 import time
 from dataclasses import dataclass
 
@@ -437,14 +438,21 @@ def render_detail(volume: Volume, camera: Camera, params: RenderParams, config: 
         part = _lib.vx_partition(int(partition[0]), int(partition[1]))
     _lib.call("vx_render", dev.handle, C.byref(rs), C.byref(rp), C.byref(fc),
               C.byref(part) if part is not None else None, C.byref(out), exc_type=RenderError)
-    names = ("lookups", "skips", "chunks_skipped", "unused", "sample_groups",
-             "filter_evals", "hits", "iterations")
-    ms = C.c_float(-1.0)
-    _lib.call("vx_last_render_ms", C.byref(ms))
-    return FrameDetail(device_ms=ms.value if ms.value >= 0.0 else None, pixels=pixels, hit_voxel=vox, hit_t=t, hit_value=val, intensity=inten,
-                       image_hist=small[:256], hit_count=int(small[256]), samples=int(small[257]),
-                       diag=dict(zip(names, (int(v) for v in small[258:266])))
+    device_ms = None
+    if getattr(_timing, "on", False):
+        ms = C.c_float(-1.0)
+        _lib.call("vx_last_render_ms", C.byref(ms))
+        device_ms = ms.value if ms.value >= 0.0 else None
+    return FrameDetail(device_ms=device_ms, pixels=pixels, hit_voxel=vox, hit_t=t,
+                       hit_value=val, intensity=inten, image_hist=small[:256],
+                       hit_count=int(small[256]), samples=int(small[257]),
+                       diag=dict(zip(_DIAG_NAMES, (int(v) for v in small[258:266])))
                        if diagnostics else None)
+
+
+_DIAG_NAMES = ("lookups", "skips", "chunks_skipped", "unused", "sample_groups",
+               "filter_evals", "hits", "iterations")
+_timing = threading.local()  # frame_timing() state of this thread (mirrors the C side)
 
 
 class frame_timing:
@@ -453,10 +461,12 @@ class frame_timing:
 
     def __enter__(self):
         _lib.call("vx_set_frame_timing", 1)
+        _timing.on = True
         return self
 
     def __exit__(self, *exc):
         _lib.call("vx_set_frame_timing", 0)
+        _timing.on = False
         return False
 
 

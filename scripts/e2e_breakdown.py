@@ -22,7 +22,7 @@ cfg = vx.FilterConfig(kind=vx.FilterKind.LOCAL_CLUSTER).resolve_threshold(h)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
 
-def per_frame(fn, reps=50, do_flush=True):
+def per_frame(fn, reps=50, do_flush=True, dist=False):
     out = []
     for i in range(reps + 5):
         if do_flush:
@@ -33,6 +33,10 @@ def per_frame(fn, reps=50, do_flush=True):
         t1 = time.perf_counter()
         if i >= 5:
             out.append((t1 - t0) * 1e3)
+    if dist:
+        q = sorted(out)
+        return (f"median {statistics.median(q):.4f} mean {statistics.mean(q):.4f} "
+                f"p10 {q[len(q) // 10]:.4f} p90 {q[9 * len(q) // 10]:.4f} max {q[-1]:.4f}")
     return statistics.median(out)
 
 
@@ -66,3 +70,7 @@ def devonly():
 for name, fn in [("render_frame", lambda: vx.render_frame(v, cam, p, cfg, h)), ("bare vx_render", bare),
                  ("device launch+sync", devonly)]:
     print(f"{name:22s} flushed {per_frame(fn):.4f} ms   warm {per_frame(fn, do_flush=False):.4f} ms")
+
+for name, fn in [("render_frame", lambda: vx.render_frame(v, cam, p, cfg, h)), ("bare vx_render", bare),
+                 ("device launch+sync", devonly)]:
+    print(f"{name:22s} flushed x200: {per_frame(fn, reps=200, dist=True)}")
