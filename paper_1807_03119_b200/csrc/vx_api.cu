@@ -210,9 +210,26 @@ int vx_volume_finish(vx_volume* v, const uint8_t* compact_dev, cudaStream_t s) {
   if (rc) return rc;
   rc = vx_launch_cell_max(v, s);
   if (rc) return rc;
-  VX_CUDA(cudaMemcpyAsync(v->counts, dcounts, 256 * 8, cudaMemcpyDeviceToHost, s));
+  uint64_t th[257];
+  VX_CUDA(cudaMemcpyAsync(th, dcounts, 257 * 8, cudaMemcpyDeviceToHost, s));
   VX_CUDA(cudaFreeAsync(dcounts, s));
   VX_CUDA(cudaStreamSynchronize(s));
+  memcpy(v->counts, th, 256 * 8);
+  // Ready the first frame: the default filter setting thresholds at the
+  // Otsu level, so its candidate distance map (thr = T) is built now, and
+  // the frame kernels are loaded (~1 ms of GPU work and the lazy module
+  // loads, out of the first frame; VOXB200_PREPARE=0 skips both).
+  static const bool prepare = [] {
+    const char* e = getenv("VOXB200_PREPARE");
+    return !e || atoi(e) != 0;
+  }();
+  if (prepare) {
+    int32_t T;
+    memcpy(&T, &th[256], 4);
+    const uint8_t* m = nullptr;
+    if (T > 0 && T <= 255 && (rc = vx_get_dist_map(v, T, &m, s))) return rc;
+    if ((rc = vx_preload_render_kernels())) return rc;
+  }
   return VX_OK;
 }
 

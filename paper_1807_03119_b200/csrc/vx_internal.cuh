@@ -124,6 +124,7 @@ int vx_launch_phantom(uint8_t* dst, int64_t row_pitch, int64_t plane_pitch, int6
                       int64_t ny, int64_t nz, const double* shapes, int64_t n_shapes,
                       double noise_sigma, uint64_t noise_seed, const int64_t* spot_idx,
                       int64_t n_spots, int32_t spot_intensity, cudaStream_t s);
+int vx_preload_render_kernels();
 int vx_volume_alloc(int64_t nx, int64_t ny, int64_t nz, vx_volume** out);
 int vx_volume_finish(vx_volume* v, const uint8_t* compact_dev, cudaStream_t s);
 

@@ -116,12 +116,14 @@ struct RenderArgs {
   int rank, world, tiles_x, n_tiles;
   // adaptive tile order (nullable): block b renders owned tile order[b]
   // and records its duration in tile_cost[owned tile] for the next frame
-  // order[owned_tiles] holds H: the first H tiles of the order (the
-  // heaviest) are rendered by two blocks each with every ray split in two
-  // segments; the launch has owned_tiles + split_max blocks
+  // order[owned_tiles..+2] holds H8, H4, H2: the first tiles of the order
+  // (the heaviest) are rendered by 8, 4 or 2 blocks each with every ray
+  // split in as many segments; the launch has owned_tiles + split_max
+  // blocks.  A ray is split only with >= split_min_chunks chunks per segment
+  // (8; 1 under the tests' split-everything schedule).
   const uint32_t* tile_order;
   uint32_t* tile_cost;
-  int owned_tiles, split_max;
+  int owned_tiles, split_max, split_min_chunks;
   double lut[256];
 };
 
@@ -893,27 +895,35 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
   // (heaviest first, so the longest warps start at once), else the deal.
   // nseg > 1: a split block -- part `part` of the tile (16/nseg rows), each
   // warp 32/nseg rays with lanes l, l+32/nseg, ... marching the nseg
-  // consecutive segments of one ray.  The first H4 tiles of the order are
-  // split in 4 (four blocks each), the next H2 in 2, the rest whole.
+  // consecutive segments of one ray.  The first H8 tiles of the order are
+  // split in 8 (eight blocks each), the next H4 in 4, the next H2 in 2, the
+  // rest whole.
   int owned, nseg = 1, part = 0;
   if (!BUDGET && kSplitRays && a.tile_order) {
     // capped by this launch's reserve: the order may come from a frame of
     // another filter setting with another split cap
-    int H4 = (int)a.tile_order[a.owned_tiles];
-    int H2 = (int)a.tile_order[a.owned_tiles + 1];
-    if (3 * H4 > a.split_max) H4 = a.split_max / 3;
-    if (3 * H4 + H2 > a.split_max) H2 = a.split_max - 3 * H4;
+    int H8 = (int)a.tile_order[a.owned_tiles];
+    int H4 = (int)a.tile_order[a.owned_tiles + 1];
+    int H2 = (int)a.tile_order[a.owned_tiles + 2];
+    if (7 * H8 > a.split_max) H8 = a.split_max / 7;
+    if (7 * H8 + 3 * H4 > a.split_max) H4 = (a.split_max - 7 * H8) / 3;
+    if (7 * H8 + 3 * H4 + H2 > a.split_max) H2 = a.split_max - 7 * H8 - 3 * H4;
     const int b = (int)blockIdx.x;
-    if (b < 4 * H4) {
-      owned = (int)a.tile_order[b >> 2];
+    const int e8 = 8 * H8, e4 = e8 + 4 * H4, e2 = e4 + 2 * H2;
+    if (b < e8) {
+      owned = (int)a.tile_order[b >> 3];
+      nseg = 8;
+      part = b & 7;
+    } else if (b < e4) {
+      owned = (int)a.tile_order[H8 + ((b - e8) >> 2)];
       nseg = 4;
-      part = b & 3;
-    } else if (b < 4 * H4 + 2 * H2) {
-      owned = (int)a.tile_order[H4 + ((b - 4 * H4) >> 1)];
+      part = (b - e8) & 3;
+    } else if (b < e2) {
+      owned = (int)a.tile_order[H8 + H4 + ((b - e4) >> 1)];
       nseg = 2;
-      part = (b - 4 * H4) & 1;
-    } else if (b - 3 * H4 - H2 < a.owned_tiles) {
-      owned = (int)a.tile_order[b - 3 * H4 - H2];
+      part = (b - e4) & 1;
+    } else if (b - 7 * H8 - 3 * H4 - H2 < a.owned_tiles) {
+      owned = (int)a.tile_order[b - 7 * H8 - 3 * H4 - H2];
     } else {
       return;  // spare block (reserve not used up), whole block
     }
@@ -939,8 +949,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
   const int rpw = 32 / nseg;  // rays per warp
   const int seg = (int)(tid & 31) / rpw;
   const int ray = (int)(tid & 31) % rpw;
-  const int i = tx * kTileW + (ray & 7);
-  const int j = nseg > 1 ? ty * kTileH + part * (kTileH / nseg) + (tid >> 5) * (rpw >> 3) + (ray >> 3)
+  // split: the part's 128/nseg rays, row-major 8 wide, rpw per warp
+  const int rp = (tid >> 5) * rpw + ray;
+  const int i = tx * kTileW + (nseg > 1 ? (rp & 7) : (ray & 7));
+  const int j = nseg > 1 ? ty * kTileH + part * (kTileH / nseg) + (rp >> 3)
                          : ty * kTileH +
                                (int)(blockIdx.x % kBlocksPerTile) * (4 * kWarpsPerBlock) +
                                (int)threadIdx.y;
@@ -990,7 +1002,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
   int K = 0, done0 = 0, stop = 0;
   if (nseg > 1 && live) {
     const float nsf = __fmul_rn(__fsub_rn(R.tend, R.base), a.M.inv_s);
-    K = nsf < 8.0f * a.M.chunk * nseg ? 0 : ((int)(nsf / nseg) / a.M.chunk) * a.M.chunk;
+    K = nsf < (float)(a.split_min_chunks * a.M.chunk * nseg)
+            ? 0
+            : ((int)(nsf / nseg) / a.M.chunk) * a.M.chunk;
     if (K == 0) {
       live = seg == 0;  // too short to split: segment 0 marches it all
     } else {
@@ -1092,7 +1106,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
       g_warp_t1[w] = wt1;
       unsigned sm;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-      g_warp_sm[w] = sm;
+      // sm | nseg << 8 | part << 12 | owned tile << 16
+      g_warp_sm[w] = sm | ((unsigned)nseg << 8) | ((unsigned)part << 12) | ((unsigned)owned << 16);
     }
   }
 #endif
@@ -1134,12 +1149,21 @@ __global__ void span_max_kernel(const RayCamD C, int nx, int ny, int nz,
 
 // next frame's tile order from this frame's per-tile costs: heaviest first
 // (64 buckets, four per octave, descending; order within a bucket is
-// irrelevant, every order renders the same frame).  order[n], order[n+1] =
-// H4, H2: the leading tiles to split next frame in 4 and in 2 segments: the
-// tiles that would outlast the
-// frame's ideal length (total cost / concurrent tile slots), when the
-// heaviest took >= split_us (split_us == 0: tests, see below).  One block;
-// resets the costs.
+// irrelevant, every order renders the same frame).  order[n..n+2] = H8, H4,
+// H2: the leading tiles to split next frame in 8, 4 and 2 segments: the tiles
+// that would outlast the frame's ideal length (total cost / concurrent tile
+// slots) by 4x, 2x and 1x, when the heaviest took >= split_us (split_us == 0:
+// tests, see below).  One block; resets the costs.
+// split thresholds in eighths of the ideal frame length
+#ifndef VX_SPLIT_T2
+#define VX_SPLIT_T2 8
+#endif
+#ifndef VX_SPLIT_T4
+#define VX_SPLIT_T4 16
+#endif
+#ifndef VX_SPLIT_T8
+#define VX_SPLIT_T8 32
+#endif
 __device__ __forceinline__ int cost_bucket(unsigned c) {
   if (c < 4) return (int)c;
   const int e = 31 - __clz(c);
@@ -1178,22 +1202,26 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(uint32_t* __restrict__
   }
   __syncthreads();
   if (tid == 0) {
-    // H4: tiles >= 2x the ideal length (split in 4), H2: tiles >= the ideal
-    // (split in 2); extra blocks 3*H4 + H2 within the launch's reserve
-    unsigned h4 = 0, h2 = 0;
-    if (split_us == 0) {  // tests: a quarter of the tiles in 4, a quarter in 2
-      h4 = (unsigned)n / 4;
-      h2 = (unsigned)n / 4;
+    // H8: tiles >= 4x the ideal length (split in 8), H4: >= 2x (in 4), H2:
+    // >= the ideal (in 2); extra blocks 7*H8 + 3*H4 + H2 within the launch's
+    // reserve
+    unsigned h8 = 0, h4 = 0, h2 = 0;
+    if (split_us == 0) {  // tests: 1/16 of the tiles in 8, 1/8 in 4, 1/8 in 2
+      h8 = (unsigned)n / 16;  // (15/16 n extra blocks: fits a reserve of n)
+      h4 = (unsigned)n / 8;
+      h2 = (unsigned)n / 8;
     } else if (top >= (unsigned)split_us) {
       const unsigned long long ideal = total / (unsigned long long)(slots > 0 ? slots : 1);
-      const int b2 = cost_bucket((unsigned)min(ideal, 0xffffffffull));
-      const int b4 = cost_bucket((unsigned)min(2 * ideal, 0xffffffffull));
-      for (int b = 63; b >= b2; --b) (b >= b4 ? h4 : h2) += cnt[b];
+      const int b2 = cost_bucket((unsigned)min(ideal * VX_SPLIT_T2 / 8, 0xffffffffull));
+      const int b4 = cost_bucket((unsigned)min(ideal * VX_SPLIT_T4 / 8, 0xffffffffull));
+      const int b8 = cost_bucket((unsigned)min(ideal * VX_SPLIT_T8 / 8, 0xffffffffull));
+      for (int b = 63; b >= b2; --b) (b >= b8 ? h8 : (b >= b4 ? h4 : h2)) += cnt[b];
     }
     // uncapped demand: the launch caps it to its reserve, and the host sizes
     // the next reserve from it
-    order[n] = h4;
-    order[n + 1] = h2;
+    order[n] = h8;
+    order[n + 1] = h4;
+    order[n + 2] = h2;
     unsigned run = 0;
     for (int b = 63; b >= 0; --b) {
       const unsigned c = cnt[b];
@@ -1503,7 +1531,34 @@ __global__ void __launch_bounds__(256) accept_cells_kernel(VolView V, FiltD F, A
     cz = (int)(ci / ((long long)A.ncx * A.ncy));
     cand = __ldg(A.cmax + (cz * A.csz + cy * A.csy + cx)) >= A.thr;
   }
-  unsigned todo = __ballot_sync(full, cand);
+  // Round 1, one cell per lane: the filter at the cell's first voxel (in
+  // the 64-voxel order below) that reaches thr.  Interior cells of an object
+  // are accepted here with one evaluation per cell, all lanes in parallel.
+  bool unresolved = false;
+  if (cand) {
+    const int x0 = cx * VX_CELL, y0 = cy * VX_CELL, z0 = cz * VX_CELL;
+    int fq = -1;
+    for (int q = 0; q < 16 && fq < 0; ++q) {
+      const int y = y0 + (q & 3), z = z0 + (q >> 2);
+      if (y >= V.ny || z >= V.nz) continue;
+      // 4-voxel rows are 4-byte aligned (origin and pitches are multiples of 16)
+      const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(V.origin + z * V.sz + y * V.sy + x0));
+      for (int xx = 0; xx < 4; ++xx)
+        if (x0 + xx < V.nx && (int)((w >> (8 * xx)) & 0xffu) >= A.thr) {
+          fq = 4 * q + xx;
+          break;
+        }
+    }
+    if (fq >= 0) {
+      if (filter_value<KIND, CHECKED>(V, F, lut, x0 + (fq & 3), y0 + ((fq >> 2) & 3), z0 + (fq >> 4)) >=
+          A.T)
+        A.occ[(int64_t)cz * A.csz + (int64_t)cy * A.csy + cx] = 255;
+      else
+        unresolved = true;  // another voxel of the cell may still pass
+    }
+  }
+  // Round 2: cells whose first voxel failed, 32 voxels at a time by the warp
+  unsigned todo = __ballot_sync(full, unresolved);
   while (todo) {
     const int src = __ffs(todo) - 1;
     todo &= todo - 1;
@@ -1552,6 +1607,17 @@ struct Scratch {
 };
 
 }  // namespace
+
+// Force the lazy module loader to bring in the frame kernels of the paper's
+// filter (and the unfiltered one) now, at volume creation, instead of inside
+// the first frame (cudaFuncGetAttributes loads the function).
+int vx_preload_render_kernels() {
+  cudaFuncAttributes fa;
+  VX_CUDA(cudaFuncGetAttributes(&fa, raycast_kernel<VX_FILTER_LOCAL_CLUSTER, false, false, false>));
+  VX_CUDA(cudaFuncGetAttributes(&fa, raycast_kernel<VX_FILTER_NONE, false, false, false>));
+  VX_CUDA(cudaFuncGetAttributes(&fa, tile_order_kernel));
+  return VX_OK;
+}
 
 // Accepted-cell distance map for the render's filter setting (nullptr: use
 // the raw candidate map).  Policy: a setting seen for the first time renders
@@ -1663,12 +1729,13 @@ static int get_accept_map(vx_volume* v, const RenderArgs& a, bool checked, const
 // setting the frame's tail.  Any order renders the same frame (tiles are
 // independent), so stale costs only cost time.  Per calling thread, keyed by
 // (volume, frame size, partition, stream); VOXB200_TILE_ORDER=0 disables.
+constexpr int kSchedHdr = 4;  // u32 slots between order[] and cost[]
 struct TileSched {
   const void* vol = nullptr;
   int w = 0, h = 0, rank = 0, world = 0, grid = 0;
   cudaStream_t stream = nullptr;
-  uint32_t* buf = nullptr;  // order[grid], H4, H2, then cost[grid]
-  uint32_t* demand = nullptr;  // pinned host copy of H4, H2
+  uint32_t* buf = nullptr;  // order[grid], H8, H4, H2, pad, then cost[grid]
+  uint32_t* demand = nullptr;  // pinned host copy of H8, H4, H2, pad
   bool valid = false;
 };
 static thread_local TileSched tl_sched;
@@ -1712,10 +1779,10 @@ static int tile_sched(vx_volume* vol, const vx_ray_setup* rs, int rank, int worl
       VX_CUDA(cudaFree(t.buf));
       t.buf = nullptr;
     }
-    VX_CUDA(cudaMalloc(&t.buf, (size_t)grid * 8 + 8));
-    if (!t.demand) VX_CUDA(cudaHostAlloc(&t.demand, 8, cudaHostAllocDefault));
-    t.demand[0] = t.demand[1] = 0;
-    VX_CUDA(cudaMemsetAsync(t.buf + grid + 2, 0, (size_t)grid * 4, s));
+    VX_CUDA(cudaMalloc(&t.buf, (size_t)grid * 8 + 4 * kSchedHdr));
+    if (!t.demand) VX_CUDA(cudaHostAlloc(&t.demand, 4 * kSchedHdr, cudaHostAllocDefault));
+    for (int k = 0; k < kSchedHdr; ++k) t.demand[k] = 0;
+    VX_CUDA(cudaMemsetAsync(t.buf + grid + kSchedHdr, 0, (size_t)grid * 4, s));
     t.vol = vol;
     t.w = rs->width;
     t.h = rs->height;
@@ -1739,13 +1806,13 @@ struct OrderJob {
 static int order_tiles(const OrderJob& j, cudaStream_t s) {
   if (!j.ts) return VX_OK;
   TileSched* ts = j.ts;
-  tile_order_kernel<<<1, 1024, 0, s>>>(ts->buf + j.grid + 2, ts->buf, j.grid,
+  tile_order_kernel<<<1, 1024, 0, s>>>(ts->buf + j.grid + kSchedHdr, ts->buf, j.grid,
                                        g_sched_split_us.load(),
                                        vx_sm_count() * (VX_RAYCAST_MIN_WARPS / kWarpsPerBlock));
   VX_CHECK_LAUNCH();
   // the split demand, read back without a sync: it sizes a later frame's
   // reserve of extra blocks (a stale value only costs time)
-  VX_CUDA(cudaMemcpyAsync(ts->demand, ts->buf + j.grid, 8, cudaMemcpyDeviceToHost, s));
+  VX_CUDA(cudaMemcpyAsync(ts->demand, ts->buf + j.grid, 4 * kSchedHdr, cudaMemcpyDeviceToHost, s));
   ts->valid = true;
   return VX_OK;
 }
@@ -1813,14 +1880,15 @@ static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_p
   // (C3 entropy 0.245 -> 0.345 ms measured), so it is not split.  The
   // reserve of extra blocks follows the last known demand (spare blocks
   // still cost a launch slot each).
+  a.split_min_chunks = g_sched_split_us.load() == 0 ? 1 : 8;
   a.split_max = a.F.kind == VX_FILTER_ENTROPY && g_sched_split_us.load() != 0
                     ? 0
                     : grid / g_sched_split_div.load();
   if (ts) {
-    a.tile_cost = ts->buf + grid + 2;
+    a.tile_cost = ts->buf + grid + kSchedHdr;
     a.tile_order = ts->valid ? ts->buf : nullptr;
     if (ts->valid) {
-      const long long want = 3ll * ts->demand[0] + ts->demand[1];
+      const long long want = 7ll * ts->demand[0] + 3ll * ts->demand[1] + ts->demand[2];
       const long long reserve = want + want / 4 + 32;
       if (reserve < a.split_max) a.split_max = (int)reserve;
     }

@@ -36,35 +36,93 @@ __global__ void brick_max_kernel(const uint8_t* __restrict__ origin, int64_t sy,
   bmax_origin[(int64_t)bz * bsz + (int64_t)by * bsy + bx] = (uint8_t)m;
 }
 
-// Chebyshev distance transform on the brick grid, separable min-max passes:
-// D(b) = min_o max_i |b_i - o_i| over occupied o = min_oz max(|dz|, min_oy
-// max(|dy|, min_ox |dx|)).  Out-of-map cells are unoccupied; capped.
-__global__ void dist_pass_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
-                                 int mx, int my, int mz, int axis, int thr, int first, int cap) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t n = (int64_t)mx * my * mz;
-  if (c >= n) return;
-  const int ix = (int)(c % mx);
-  const int iy = (int)((c / mx) % my);
-  const int iz = (int)(c / ((int64_t)mx * my));
-  const int len = axis == 0 ? mx : (axis == 1 ? my : mz);
-  const int pos = axis == 0 ? ix : (axis == 1 ? iy : iz);
-  const int64_t stride = axis == 0 ? 1 : (axis == 1 ? (int64_t)mx : (int64_t)mx * my);
-  int best = cap;
-  for (int k = -cap + 1; k < cap; ++k) {
-    const int q = pos + k;
-    if (q < 0 || q >= len) continue;
-    const int ak = k < 0 ? -k : k;
-    if (ak >= best) continue;
-    const uint8_t v = src[c + (int64_t)k * stride];
-    int val;
-    if (first)
-      val = v >= thr ? ak : cap;
-    else
-      val = v > ak ? v : ak;
-    if (val < best) best = val;
+// Chebyshev distance transform on the brick / cell grid, separable min-max
+// passes: D(b) = min_o max_i |b_i - o_i| over occupied o = min_oz max(|dz|,
+// min_oy max(|dy|, min_ox |dx|)).  Out-of-map cells are unoccupied; capped.
+//
+// Pass 1 (x, thresholding): the 1D distance to the nearest occupied cell of
+// the row, min(cap, forward and backward sweeps) -- O(1) per cell.  Rows of
+// the flattened (z, y) index are contiguous, so a block stages 64 whole rows
+// with coalesced loads and each thread sweeps one row in shared memory.
+// Passes 2-3 (y, z): D(l) = min_a max(v(l +- a), a) over a < cap; each cell
+// scans outward and stops once a >= its best (later terms are >= a).  A block
+// stages 128 neighbouring x-columns (coalesced 128-byte row segments) along
+// the whole line; each lane carries 4 columns packed in one 32-bit word and
+// evaluates them together with byte-SIMD max/min (__vmaxu4 / __vminu4).
+// (One thread per cell on global memory took ~0.95 ms per pass on the 258^3
+// cell map of a 1024^3 volume.)
+constexpr int kRowsPerBlock = 64;
+
+__global__ void __launch_bounds__(kRowsPerBlock) dist_first_x_kernel(
+    const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int mx, int64_t rows, int thr,
+    int cap) {
+  extern __shared__ uint8_t rowbuf[];
+  const int pitch = mx | 1;  // odd pitch: threads sweeping rows hit distinct banks
+  const int64_t r0 = (int64_t)blockIdx.x * kRowsPerBlock;
+  const int nr = (int)min((int64_t)kRowsPerBlock, rows - r0);
+  const uint8_t* s = src + r0 * mx;
+  for (int i = threadIdx.x; i < nr * mx; i += blockDim.x) rowbuf[(i / mx) * pitch + i % mx] = s[i];
+  __syncthreads();
+  if ((int)threadIdx.x < nr) {
+    uint8_t* L = rowbuf + threadIdx.x * pitch;
+    int last = -(1 << 20);
+    for (int x = 0; x < mx; ++x) {  // forward: distance to the last occupied cell
+      if (L[x] >= thr) last = x;
+      L[x] = (uint8_t)min(cap, x - last);
+    }
+    int next = 1 << 20;
+    for (int x = mx - 1; x >= 0; --x) {  // backward, and the minimum of both
+      if (L[x] == 0) next = x;
+      L[x] = (uint8_t)min((int)L[x], min(cap, next - x));
+    }
   }
-  dst[c] = (uint8_t)best;
+  __syncthreads();
+  uint8_t* d = dst + r0 * mx;
+  for (int i = threadIdx.x; i < nr * mx; i += blockDim.x) d[i] = rowbuf[(i / mx) * pitch + i % mx];
+}
+
+template <int AXIS>
+__global__ void __launch_bounds__(256) dist_minmax_kernel(const uint8_t* __restrict__ src,
+                                                          uint8_t* __restrict__ dst, int mx,
+                                                          int my, int mz, int cap) {
+  extern __shared__ uint32_t cols[];  // [n][32] words = 128 x-columns per position
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int n = AXIS == 1 ? my : mz;
+  const int x0 = blockIdx.x * 128 + 4 * tx;
+  const int64_t stride = AXIS == 1 ? (int64_t)mx : (int64_t)mx * my;
+  const int64_t base = AXIS == 1 ? (int64_t)blockIdx.y * mx * my : (int64_t)blockIdx.y * mx;
+  const int nx = min(4, mx - x0);  // columns of this lane inside the map
+  for (int l = ty; l < n; l += 8) {
+    uint32_t w = 0;
+    if (nx > 0) {
+      const uint8_t* p = src + base + l * stride + x0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) w |= (uint32_t)(c < nx ? p[c] : 0) << (8 * c);
+    }
+    cols[l * 32 + tx] = w;
+  }
+  __syncthreads();
+  if (nx <= 0) return;
+  const uint32_t C4 = (uint32_t)cap * 0x01010101u;
+  for (int l = ty; l < n; l += 8) {
+    uint32_t best = __vminu4(cols[l * 32 + tx], C4);
+    for (int a = 1; a < cap; ++a) {
+      const uint32_t A = (uint32_t)a * 0x01010101u;
+      if (!__vcmpgtu4(best, A)) break;  // every column's best <= a already
+      if (l - a >= 0) best = __vminu4(best, __vmaxu4(cols[(l - a) * 32 + tx], A));
+      if (l + a < n) best = __vminu4(best, __vmaxu4(cols[(l + a) * 32 + tx], A));
+    }
+    uint8_t* p = dst + base + l * stride + x0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (c < nx) p[c] = (uint8_t)(best >> (8 * c));
+  }
+}
+
+static int smem_opt_in(const void* fn, size_t smem) {
+  if (smem > 48 * 1024)
+    VX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  return VX_OK;
 }
 
 // one thread per VX_CELL^3 cell (4^3: 4-byte aligned rows of 4 voxels)
@@ -180,12 +238,21 @@ static int dist_transform(const uint8_t* maxmap, uint8_t* out, int mx, int my, i
   const int64_t n = (int64_t)mx * my * mz;
   uint8_t* tmp = nullptr;
   VX_CUDA(vx_malloc_async(&tmp, n, s));
-  const unsigned g = (unsigned)((n + 255) / 256);
-  dist_pass_kernel<<<g, 256, 0, s>>>(maxmap, out, mx, my, mz, 0, thr, 1, cap);
+  const int64_t rows = (int64_t)my * mz;
+  const size_t s0 = (size_t)kRowsPerBlock * (mx | 1);
+  int rc = smem_opt_in((const void*)dist_first_x_kernel, s0);
+  if (rc) return rc;
+  dist_first_x_kernel<<<(unsigned)((rows + kRowsPerBlock - 1) / kRowsPerBlock), kRowsPerBlock, s0,
+                        s>>>(maxmap, out, mx, rows, thr, cap);
   VX_CHECK_LAUNCH();
-  dist_pass_kernel<<<g, 256, 0, s>>>(out, tmp, mx, my, mz, 1, thr, 0, cap);
+  const dim3 blk(32, 8);
+  const unsigned gx = (unsigned)((mx + 127) / 128);
+  const size_t s1 = (size_t)128 * my, s2 = (size_t)128 * mz;
+  if ((rc = smem_opt_in((const void*)dist_minmax_kernel<1>, s1))) return rc;
+  dist_minmax_kernel<1><<<dim3(gx, (unsigned)mz), blk, s1, s>>>(out, tmp, mx, my, mz, cap);
   VX_CHECK_LAUNCH();
-  dist_pass_kernel<<<g, 256, 0, s>>>(tmp, out, mx, my, mz, 2, thr, 0, cap);
+  if ((rc = smem_opt_in((const void*)dist_minmax_kernel<2>, s2))) return rc;
+  dist_minmax_kernel<2><<<dim3(gx, (unsigned)my), blk, s2, s>>>(tmp, out, mx, my, mz, cap);
   VX_CHECK_LAUNCH();
   VX_CUDA(cudaFreeAsync(tmp, s));
   return VX_OK;

@@ -1,5 +1,9 @@
 """Per-warp timeline of one K4 frame (debug build with -DVX_WARP_TIMING):
-    VOXB200_LIB=.../libvoxb200_wt.so python scripts/warp_times.py [n] [kind]"""
+    VOXB200_LIB=.../libvoxb200_wt.so python scripts/warp_times.py [n] [kind] [W]
+
+The timed frame is a diagnostics frame (same schedule: tile order + split
+rays), so each warp's timing, tile, segment count and march counters come
+from the same launch."""
 import ctypes as C, os, sys
 sys.path.insert(0, os.getcwd())
 import numpy as np
@@ -20,49 +24,42 @@ object.__setattr__(v, "_content_hash", "x")
 cam = vx.orbit_camera(v)
 p = vx.RenderParams(width=W, height=W)
 cfg = vx.FilterConfig(kind=vx.FilterKind.from_name(kind)).resolve_threshold(h)
-for _ in range(3):
-    d = render_detail(v, cam, p, cfg, h)
-nw = W * W // 32
+for _ in range(4):
+    d = render_detail(v, cam, p, cfg, h, diagnostics=True)
+nmax = 2 * W * W // 32
 lib = _lib.load()
-t0 = np.zeros(nw, np.uint64); t1 = np.zeros(nw, np.uint64); sm = np.zeros(nw, np.uint32)
+t0 = np.zeros(nmax, np.uint64); t1 = np.zeros(nmax, np.uint64); info = np.zeros(nmax, np.uint32)
 lib.vx_debug_warp_times(C.c_void_p(t0.ctypes.data), C.c_void_p(t1.ctypes.data),
-                        C.c_void_p(sm.ctypes.data), nw)
+                        C.c_void_p(info.ctypes.data), nmax)
+dg = np.zeros(nmax * 9, np.uint32)
+lib.vx_debug_warp_diag(C.c_void_p(dg.ctypes.data), nmax)
+dg = dg.reshape(nmax, 9)
+# warps of this frame only (spare blocks of the reserve leave no record)
+keep = (t0 > 0) & (t0.astype(np.float64) >= float(t0.max()) - 5e6)
+idx = np.nonzero(keep)[0]
+t0, t1, info, dg = t0[keep], t1[keep], info[keep], dg[keep]
+sm, nseg, part, tile = info & 0xff, (info >> 8) & 0xf, (info >> 12) & 0xf, info >> 16
 base = t0.min()
 s = (t0 - base).astype(np.float64) / 1e3
 e = (t1 - base).astype(np.float64) / 1e3
 dur = e - s
-print(f"kernel span {e.max():.1f} us; warps {nw}; dur p50 {np.median(dur):.2f} p90 {np.percentile(dur,90):.2f} "
-      f"p99 {np.percentile(dur,99):.2f} max {dur.max():.2f} us; sum {dur.sum()/1e3:.1f} ms-warp")
-print(f"ideal (sum / (148*32 slots)) {dur.sum()/(148*32):.1f} us; last warp start {s.max():.1f} us")
-busy = np.zeros(sm.max() + 1)
-end = np.zeros(sm.max() + 1)
-for k in range(len(busy)):
-    m = sm == k
-    end[k] = e[m].max() if m.any() else 0
+print(f"kernel span {e.max():.1f} us; warps {len(dur)}; dur p50 {np.median(dur):.2f} p90 "
+      f"{np.percentile(dur, 90):.2f} p99 {np.percentile(dur, 99):.2f} max {dur.max():.2f} us; "
+      f"sum {dur.sum() / 1e3:.1f} ms-warp")
+print(f"ideal (sum / (148*32 slots)) {dur.sum() / (148 * 32):.1f} us; last warp start {s.max():.1f} us")
+for k in (8, 4, 2, 1):
+    m = nseg == k
+    if m.any():
+        print(f"  nseg {k}: {m.sum()} warps ({len(np.unique(tile[m]))} tiles), dur max {dur[m].max():.1f} "
+              f"p50 {np.median(dur[m]):.1f} us, start max {s[m].max():.1f} us")
+end = np.array([e[sm == k].max() for k in np.unique(sm)])
 print(f"per-SM last end: min {end.min():.1f} median {np.median(end):.1f} max {end.max():.1f} us")
-# warp index -> tile position: block b = w // 4 covers tile b (8x16), warp w%4 the rows 4*(w%4)..
-tiles_x = W // 8
-b = np.arange(nw) // 4
-ty, tx = b // tiles_x, b % tiles_x
-row = ty * 16 + (np.arange(nw) % 4) * 4
-col = tx * 8
-top = np.argsort(-dur)[:6]
-for w in top:
-    print(f"  warp {w}: dur {dur[w]:.1f} us start {s[w]:.1f} rows {row[w]}..{row[w]+3} cols {col[w]}..{col[w]+7} sm {sm[w]}")
-# duration by image band (64 rows)
-img = np.zeros((W // 4, W // 8))
-img[row // 4, col // 8] = dur
-bands = img.reshape(W // 64, 16, W // 8).sum(axis=(1, 2)) / 1e3
-print("ms-warp per 64-row band:", " ".join(f"{x:.1f}" for x in bands))
-np.save("gpurun_out/warp_dur.npy", img)
-# per-warp march statistics (diagnostics frame; the warp deal is identical)
-d = render_detail(v, cam, p, cfg, h, diagnostics=True)
-dg = np.zeros(nw * 9, np.uint32)
-lib.vx_debug_warp_diag(C.c_void_p(dg.ctypes.data), nw)
-dg = dg.reshape(nw, 9)
 names = ("lookups", "inchunk", "chunks", "unused", "groups", "filters", "hits", "iters", "max_iters")
-print("slowest warps (timing frame) statistics (diag frame):")
-for w in top[:8]:
-    print(f"  warp {w}: " + " ".join(f"{k}={int(x)}" for k, x in zip(names, dg[w])))
+top = np.argsort(-dur)[:8]
+tiles_x = W // 8
+for w in top:
+    ty, tx = divmod(int(tile[w]), tiles_x)
+    print(f"  warp {idx[w]}: dur {dur[w]:.1f} us start {s[w]:.1f} tile ({ty * 16},{tx * 8}) nseg {nseg[w]} "
+          f"part {part[w]} sm {sm[w]} | " + " ".join(f"{k}={int(x)}" for k, x in zip(names, dg[w])))
 med = np.median(dg, axis=0)
 print("  median warp: " + " ".join(f"{k}={x:.0f}" for k, x in zip(names, med)))

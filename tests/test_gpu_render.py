@@ -325,9 +325,10 @@ def test_sharded_api_single_rank_nccl(vx, small_sphere_volume, small_sphere_hist
 
 @pytest.fixture
 def split_everything():
-    """Schedule every frame's tiles by cost and split every ray of every tile
-    in two segments (production only splits the heaviest tiles of big
-    frames); restored afterwards."""
+    """Schedule every frame's tiles by cost and split the rays of 1/16 of the
+    tiles in 8 segments, 1/8 in 4 and 1/8 in 2, down to one
+    chunk per segment (production only splits the heaviest tiles of big
+    frames, and only rays of >= 8 chunks per segment); restored afterwards."""
     from paper_1807_03119_b200 import _lib
 
     _lib.call("vx_set_schedule", 1, 0, 0, 1)
@@ -336,8 +337,8 @@ def split_everything():
 
 
 def test_split_rays_and_tile_order_match_oracle(vx, oracle, split_everything):
-    """Frames 2+ of a setting run with the cost-ordered tiles and two-segment
-    rays (segment 1 starts from the exact chunk base of its first sample):
+    """Frames 2+ of a setting run with the cost-ordered tiles and 8/4/2-segment
+    rays (segment s starts from the exact chunk base of its first sample):
     hit voxels and pixels equal the oracle's, for every filter and steps that
     exercise the chunk rule."""
     from paper_1807_03119_b200.render import render_detail

@@ -135,6 +135,53 @@ def _brute_distance(bmax_occ: np.ndarray, cap: int) -> np.ndarray:
     return out
 
 
+def _separable_distance(occ: np.ndarray, cap: int) -> np.ndarray:
+    """Chebyshev distance (capped) by the separable min-max passes, in numpy."""
+    big = np.int64(cap)
+    d = np.where(occ, 0, big).astype(np.int64)
+    for axis in (2, 1, 0):  # x, y, z
+        n = d.shape[axis]
+        out = np.full(d.shape, big, dtype=np.int64)
+        for k in range(-cap + 1, cap):
+            if abs(k) >= n:
+                continue
+            src = [slice(None)] * 3
+            dst = [slice(None)] * 3
+            if k >= 0:
+                src[axis], dst[axis] = slice(k, n), slice(0, n - k)
+            else:
+                src[axis], dst[axis] = slice(0, n + k), slice(-k, n)
+            out[tuple(dst)] = np.minimum(out[tuple(dst)], np.maximum(d[tuple(src)], abs(k)))
+        d = out
+    return d
+
+
+def test_distance_map_long_lines(vx):
+    """Fine (4^3, cap 32) and coarse (8^3, cap 24) maps of a volume whose cell
+    lines are longer than twice the cap, against a numpy restatement; sparse
+    points, a slab and a line of occupied cells."""
+    from paper_1807_03119_b200.volume import device_volume
+
+    rs = np.random.default_rng(7)
+    nz, ny, nx = 300, 272, 264
+    data = rs.integers(0, 90, (nz, ny, nx), dtype=np.uint8)
+    for _ in range(25):
+        data[rs.integers(0, nz), rs.integers(0, ny), rs.integers(0, nx)] = 210
+    data[150:160, 20:30, 100:240] = 180
+    data[5, 250, :] = 255
+    dv = device_volume(vx.Volume(dims=(nx, ny, nz), data=data))
+    for c, cap, level in ((4, 32, 1), (8, 24, 0)):
+        ncz, ncy, ncx = (nz + c - 1) // c, (ny + c - 1) // c, (nx + c - 1) // c
+        pad = np.zeros((ncz * c, ncy * c, ncx * c), dtype=np.uint8)
+        pad[:nz, :ny, :nx] = data
+        cmax = pad.reshape(ncz, c, ncy, c, ncx, c).max(axis=(1, 3, 5))
+        for thr in (100, 200):
+            occ = np.zeros((ncz + 2, ncy + 2, ncx + 2), dtype=bool)
+            occ[1:-1, 1:-1, 1:-1] = cmax >= thr
+            got = dv.distance_map(thr, level=level).astype(np.int64)
+            assert np.array_equal(got, _separable_distance(occ, cap)), (c, thr)
+
+
 def test_distance_map_is_exact_chebyshev(vx):
     from paper_1807_03119_b200.volume import device_volume
 
