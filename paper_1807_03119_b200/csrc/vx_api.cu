@@ -168,7 +168,7 @@ int vx_volume_alloc(int64_t nx, int64_t ny, int64_t nz, vx_volume** out) {
   v->cmap_bytes = (uint64_t)v->csz * (v->ncz + 2);
   for (auto& d : v->dist) {
     d.thr = -1;
-    d.map = nullptr;
+    d.map = nullptr;  // slots assigned below
     d.stamp = 0;
   }
   cudaError_t e = cudaMalloc(&v->alloc, v->alloc_bytes);
@@ -176,13 +176,16 @@ int vx_volume_alloc(int64_t nx, int64_t ny, int64_t nz, vx_volume** out) {
     delete v;
     return vx_cuda_fail(e, "cudaMalloc(volume)", __FILE__, __LINE__);
   }
-  e = cudaMalloc(&v->bmax, v->map_bytes + v->cmap_bytes);
+  const uint64_t slot = v->map_bytes + v->cmap_bytes;
+  e = cudaMalloc(&v->bmax, slot * (1 + VX_DIST_CACHE + VX_ACC_CACHE));
   if (e != cudaSuccess) {
     cudaFree(v->alloc);
     delete v;
     return vx_cuda_fail(e, "cudaMalloc(brick map)", __FILE__, __LINE__);
   }
   v->cmax = v->bmax + v->map_bytes;
+  for (int i = 0; i < VX_DIST_CACHE; ++i) v->dist[i].map = v->bmax + slot * (1 + i);
+  for (int i = 0; i < VX_ACC_CACHE; ++i) v->acc[i].map = v->bmax + slot * (1 + VX_DIST_CACHE + i);
   v->origin = v->alloc + VX_PAD * v->sz + VX_PAD * v->sy + VX_PAD;
   *out = v;
   return VX_OK;
@@ -360,10 +363,6 @@ extern "C" int vx_volume_destroy(vx_volume* v) {
   cudaGetDevice(&cur);
   if (cur != v->device) cudaSetDevice(v->device);
   cudaDeviceSynchronize();
-  for (auto& d : v->dist)
-    if (d.map) cudaFree(d.map);
-  for (auto& a : v->acc)
-    if (a.map) cudaFree(a.map);
   if (v->bmax) cudaFree(v->bmax);
   if (v->alloc) cudaFree(v->alloc);
   if (cur != v->device) cudaSetDevice(cur);
@@ -413,7 +412,7 @@ int vx_get_dist_map(vx_volume* v, int thr, const uint8_t** map_out, cudaStream_t
   std::lock_guard<std::mutex> lock(v->mu);
   ++v->stamp;
   for (auto& d : v->dist) {
-    if (d.map && d.thr == thr) {
+    if (d.thr >= 0 && d.thr == thr) {
       d.stamp = v->stamp;
       *map_out = d.map;
       return VX_OK;
@@ -421,18 +420,14 @@ int vx_get_dist_map(vx_volume* v, int thr, const uint8_t** map_out, cudaStream_t
   }
   DistEntry* victim = &v->dist[0];
   for (auto& d : v->dist) {
-    if (!d.map) {
+    if (d.thr < 0) {
       victim = &d;
       break;
     }
     if (d.stamp < victim->stamp) victim = &d;
   }
-  if (victim->map) {
-    // another thread's stream may still read the evicted map
-    VX_CUDA(cudaDeviceSynchronize());
-  } else {
-    VX_CUDA(cudaMalloc(&victim->map, v->map_bytes + v->cmap_bytes));
-  }
+  // another thread's stream may still read the evicted map
+  if (victim->thr >= 0) VX_CUDA(cudaDeviceSynchronize());
   victim->thr = -1;
   int rc = vx_launch_dist_map(v, thr, victim->map, s);
   if (rc) return rc;

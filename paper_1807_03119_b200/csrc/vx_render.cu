@@ -24,7 +24,9 @@
 // construction; disabled automatically when thr == 0 (every brick occupied).
 
 #include <atomic>
+#include <chrono>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -1611,13 +1613,39 @@ struct Scratch {
 // Force the lazy module loader to bring in the frame kernels of the paper's
 // filter (and the unfiltered one) now, at volume creation, instead of inside
 // the first frame (cudaFuncGetAttributes loads the function).
+static int demand_arena_init();
+
 int vx_preload_render_kernels() {
   cudaFuncAttributes fa;
   VX_CUDA(cudaFuncGetAttributes(&fa, raycast_kernel<VX_FILTER_LOCAL_CLUSTER, false, false, false>));
   VX_CUDA(cudaFuncGetAttributes(&fa, raycast_kernel<VX_FILTER_NONE, false, false, false>));
   VX_CUDA(cudaFuncGetAttributes(&fa, tile_order_kernel));
-  return VX_OK;
+  VX_CUDA(cudaFuncGetAttributes(&fa, accept_cells_kernel<VX_FILTER_LOCAL_CLUSTER, false>));
+  return demand_arena_init();
 }
+
+// VOXB200_TRACE=1: host wall-clock phases of vx_render on stderr (cold-path
+// diagnosis: map builds, allocations, copies)
+static bool trace_on() {
+  static const bool on = [] {
+    const char* e = getenv("VOXB200_TRACE");
+    return e && atoi(e) != 0;
+  }();
+  return on;
+}
+static double trace_us() {
+  return std::chrono::duration<double, std::micro>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+#define VX_TRACE(label, t0)                                                       \
+  do {                                                                            \
+    if (trace_on()) {                                                             \
+      const double _t = trace_us();                                               \
+      fprintf(stderr, "[vx_trace] %-18s %9.1f us\n", label, _t - (t0));          \
+      t0 = _t;                                                                    \
+    }                                                                             \
+  } while (0)
 
 // Accepted-cell distance map for the render's filter setting (nullptr: use
 // the raw candidate map).  Policy: a setting seen for the first time renders
@@ -1658,7 +1686,7 @@ static int get_accept_map(vx_volume* v, const RenderArgs& a, bool checked, const
   AccEntry* e = nullptr;
   for (auto& c : v->acc)
     if (c.valid && !memcmp(c.key, &key, sizeof(key))) e = &c;
-  if (e && e->map) {
+  if (e && e->built) {
     e->stamp = v->stamp;
     *out = e->map;
     return VX_OK;
@@ -1672,24 +1700,20 @@ static int get_accept_map(vx_volume* v, const RenderArgs& a, bool checked, const
       }
       if (c.stamp < e->stamp) e = &c;
     }
-    if (e->valid && e->map) VX_CUDA(cudaDeviceSynchronize());  // another stream may read it
+    if (e->valid && e->built) VX_CUDA(cudaDeviceSynchronize());  // another stream may read it
     e->valid = true;
+    e->built = false;
     memcpy(e->key, &key, sizeof(key));
     e->stamp = v->stamp;
-    if (mode == 1) {
-      if (e->map) {
-        cudaFree(e->map);
-        e->map = nullptr;
-      }
-      return VX_OK;  // first sight: raw map
-    }
+    if (mode == 1) return VX_OK;  // first sight: raw map
   }
-  if (!e->map) VX_CUDA(cudaMalloc(&e->map, v->map_bytes + v->cmap_bytes));
+  double tt = trace_on() ? trace_us() : 0.0;
   e->valid = false;  // until built
   uint8_t* occ = nullptr;
   VX_CUDA(vx_malloc_async(&occ, v->cmap_bytes, s));
   VX_CUDA(cudaMemsetAsync(occ, 0, v->cmap_bytes, s));
   VX_CUDA(cudaMemsetAsync(e->map, 0, v->map_bytes, s));  // coarse level unused: no skip
+  VX_TRACE("  acc scratch", tt);
   AccArgs A;
   A.cmax = v->cmax + v->csz + v->csy + 1;
   A.occ = occ + v->csz + v->csy + 1;
@@ -1712,9 +1736,12 @@ static int get_accept_map(vx_volume* v, const RenderArgs& a, bool checked, const
   int rc = vx_launch_dist_cells(v, occ, e->map + v->map_bytes, 1, s);
   if (rc) return rc;
   VX_CUDA(cudaFreeAsync(occ, s));
+  VX_TRACE("  acc launches", tt);
   // other streams may pick this map up: make it visible before publishing
   VX_CUDA(cudaStreamSynchronize(s));
+  VX_TRACE("  acc sync", tt);
   e->valid = true;
+  e->built = true;
   e->stamp = v->stamp;
   *out = e->map;
   return VX_OK;
@@ -1759,6 +1786,27 @@ extern "C" int vx_set_schedule(int32_t tile_order, int32_t min_grid_tiles, int32
   return VX_OK;
 }
 
+// page-locked split-demand slots for the per-thread schedules, carved from one
+// arena allocated with the frame kernels' preload (a cudaHostAlloc inside the
+// first frame measured ~1-3 ms)
+static std::mutex g_demand_mu;
+static uint32_t* g_demand_arena = nullptr;
+static int g_demand_used = 0;
+constexpr int kDemandSlots = 256;
+
+static int demand_arena_init() {
+  std::lock_guard<std::mutex> lk(g_demand_mu);
+  if (!g_demand_arena)
+    VX_CUDA(cudaHostAlloc(&g_demand_arena, 4 * kSchedHdr * kDemandSlots, cudaHostAllocDefault));
+  return VX_OK;
+}
+
+static uint32_t* demand_slot() {
+  std::lock_guard<std::mutex> lk(g_demand_mu);
+  if (!g_demand_arena || g_demand_used >= kDemandSlots) return nullptr;
+  return g_demand_arena + kSchedHdr * g_demand_used++;
+}
+
 static int tile_sched(vx_volume* vol, const vx_ray_setup* rs, int rank, int world, int grid,
                       cudaStream_t s, TileSched** out) {
   static const bool env_on = [] {
@@ -1776,10 +1824,12 @@ static int tile_sched(vx_volume* vol, const vx_ray_setup* rs, int rank, int worl
       t.world != world || t.grid != grid || t.stream != s || !t.buf) {
     if (t.buf) {
       VX_CUDA(cudaStreamSynchronize(t.stream));
-      VX_CUDA(cudaFree(t.buf));
+      VX_CUDA(cudaFreeAsync(t.buf, t.stream));
       t.buf = nullptr;
     }
-    VX_CUDA(cudaMalloc(&t.buf, (size_t)grid * 8 + 4 * kSchedHdr));
+    // stream-ordered pool (no device-wide cudaMalloc inside a frame)
+    VX_CUDA(vx_malloc_async(&t.buf, (size_t)grid * 8 + 4 * kSchedHdr, s));
+    if (!t.demand) t.demand = demand_slot();
     if (!t.demand) VX_CUDA(cudaHostAlloc(&t.demand, 4 * kSchedHdr, cudaHostAllocDefault));
     for (int k = 0; k < kSchedHdr; ++k) t.demand[k] = 0;
     VX_CUDA(cudaMemsetAsync(t.buf + grid + kSchedHdr, 0, (size_t)grid * 4, s));
@@ -1839,12 +1889,15 @@ static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_p
   for (int i = 0; i < 256; ++i) a.lut[i] = fc->entropy_lut[i];
   const bool checked = filter_reach(a.F) > VX_PAD - 1;
   const uint8_t* dist = nullptr;
+  double tt = trace_on() ? trace_us() : 0.0;
   if (a.M.skip) {
     a.V = vx_view(vol, nullptr);
     rc = get_accept_map(vol, a, checked, &dist, s);
     if (rc) return rc;
+    VX_TRACE("accept_map", tt);
     if (!dist) rc = vx_get_dist_map(vol, a.M.thr, &dist, s);
     if (rc) return rc;
+    VX_TRACE("dist_map", tt);
   }
   a.V = vx_view(vol, dist);
   a.O.pixels = o->pixels;
@@ -1893,11 +1946,13 @@ static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_p
       if (reserve < a.split_max) a.split_max = (int)reserve;
     }
   }
+  VX_TRACE("tile_sched", tt);
   if (checked)
     dispatch_raycast<true>(a, grid, s);
   else
     dispatch_raycast<false>(a, grid, s);
   VX_CHECK_LAUNCH();
+  VX_TRACE("k4_launch", tt);
   OrderJob job;
   job.ts = ts;
   job.grid = grid;
@@ -1997,6 +2052,7 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
     vx_set_error("image size must be >= 1x1, got %dx%d", rs->width, rs->height);
     return VX_EINVAL;
   }
+  double tv = trace_on() ? trace_us() : 0.0;
   cudaStream_t s = vx_stream();
   const size_t npx = (size_t)rs->width * rs->height;
   // device staging: pixels | hit_voxel | hit_t | hit_value | intensity | hist | counters
@@ -2017,6 +2073,7 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
   uint8_t* base = sc.get<uint8_t>();
   VX_CUDA(cudaMemsetAsync(base + o_small, 0, 256 * 8 + 3 * 8 + 8 + 64, s));
   if (part && part->world > 1) VX_CUDA(cudaMemsetAsync(base + o_pix, 0, npx, s));
+  VX_TRACE("staging", tv);
   vx_render_out d;
   d.pixels = base + o_pix;
   d.hit_voxel = out->hit_voxel ? reinterpret_cast<int32_t*>(base + o_vox) : nullptr;
@@ -2066,8 +2123,10 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
     VX_CUDA(cudaEventSynchronize(copied));
     return VX_OK;
   };
+  double tc = trace_on() ? trace_us() : 0.0;
   rc = copy_back();
   if (rc) return rc;
+  VX_TRACE("copy_back+sync", tc);
   if (timed) VX_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
   int32_t flag;
   memcpy(&flag, &small_h[258], 4);
