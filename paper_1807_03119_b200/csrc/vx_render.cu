@@ -1756,14 +1756,24 @@ static int get_accept_map(vx_volume* v, const RenderArgs& a, bool checked, const
 // setting the frame's tail.  Any order renders the same frame (tiles are
 // independent), so stale costs only cost time.  Per calling thread, keyed by
 // (volume, frame size, partition, stream); VOXB200_TILE_ORDER=0 disables.
+//
+// Double-buffered off the frame's critical path: frame k (parity p = k & 1)
+// renders in the order computed from frame k-2's costs (buf[p]) and records
+// its own costs into buf[p]; the ordering kernel for them then runs on a side
+// stream, concurrently with frame k+1 (which uses buf[p ^ 1]).  In-stream it
+// cost ~13 us of a ~160 us frame (one latency-bound block).
 constexpr int kSchedHdr = 4;  // u32 slots between order[] and cost[]
 struct TileSched {
   const void* vol = nullptr;
   int w = 0, h = 0, rank = 0, world = 0, grid = 0;
   cudaStream_t stream = nullptr;
-  uint32_t* buf = nullptr;  // order[grid], H8, H4, H2, pad, then cost[grid]
-  uint32_t* demand = nullptr;  // pinned host copy of H8, H4, H2, pad
-  bool valid = false;
+  uint32_t* buf[2] = {nullptr, nullptr};     // order[grid], H8, H4, H2, pad, then cost[grid]
+  uint32_t* demand[2] = {nullptr, nullptr};  // pinned host copies of H8, H4, H2, pad
+  bool valid[2] = {false, false};
+  int parity = 0;
+  cudaStream_t side = nullptr;  // ordering kernels
+  cudaEvent_t costs_done[2] = {nullptr, nullptr}, order_done[2] = {nullptr, nullptr};
+  int device = -1;
 };
 static thread_local TileSched tl_sched;
 
@@ -1820,19 +1830,38 @@ static int tile_sched(vx_volume* vol, const vx_ray_setup* rs, int rank, int worl
   const int min_grid = g_sched_min_grid.load() < 0 ? 4 * vx_sm_count() : g_sched_min_grid.load();
   if (!enabled || grid < min_grid) return VX_OK;
   TileSched& t = tl_sched;
-  if (t.vol != vol || t.w != rs->width || t.h != rs->height || t.rank != rank ||
-      t.world != world || t.grid != grid || t.stream != s || !t.buf) {
-    if (t.buf) {
-      VX_CUDA(cudaStreamSynchronize(t.stream));
-      VX_CUDA(cudaFreeAsync(t.buf, t.stream));
-      t.buf = nullptr;
+  int dev = 0;
+  VX_CUDA(cudaGetDevice(&dev));
+  if (t.device != dev) {  // per-thread side stream and events of this device
+    if (t.side) {
+      VX_CUDA(cudaStreamSynchronize(t.side));
+      t.vol = nullptr;  // buffers belong to the old device: rebuild below
     }
-    // stream-ordered pool (no device-wide cudaMalloc inside a frame)
-    VX_CUDA(vx_malloc_async(&t.buf, (size_t)grid * 8 + 4 * kSchedHdr, s));
-    if (!t.demand) t.demand = demand_slot();
-    if (!t.demand) VX_CUDA(cudaHostAlloc(&t.demand, 4 * kSchedHdr, cudaHostAllocDefault));
-    for (int k = 0; k < kSchedHdr; ++k) t.demand[k] = 0;
-    VX_CUDA(cudaMemsetAsync(t.buf + grid + kSchedHdr, 0, (size_t)grid * 4, s));
+    VX_CUDA(cudaStreamCreateWithFlags(&t.side, cudaStreamNonBlocking));
+    for (int p = 0; p < 2; ++p) {
+      VX_CUDA(cudaEventCreateWithFlags(&t.costs_done[p], cudaEventDisableTiming));
+      VX_CUDA(cudaEventCreateWithFlags(&t.order_done[p], cudaEventDisableTiming));
+    }
+    t.device = dev;
+    t.buf[0] = t.buf[1] = nullptr;
+  }
+  if (t.vol != vol || t.w != rs->width || t.h != rs->height || t.rank != rank ||
+      t.world != world || t.grid != grid || t.stream != s || !t.buf[0]) {
+    VX_CUDA(cudaStreamSynchronize(t.side));
+    for (int p = 0; p < 2; ++p) {
+      if (t.buf[p]) {
+        VX_CUDA(cudaStreamSynchronize(t.stream));
+        VX_CUDA(cudaFreeAsync(t.buf[p], t.stream));
+        t.buf[p] = nullptr;
+      }
+      // stream-ordered pool (no device-wide cudaMalloc inside a frame)
+      VX_CUDA(vx_malloc_async(&t.buf[p], (size_t)grid * 8 + 4 * kSchedHdr, s));
+      if (!t.demand[p]) t.demand[p] = demand_slot();
+      if (!t.demand[p]) VX_CUDA(cudaHostAlloc(&t.demand[p], 4 * kSchedHdr, cudaHostAllocDefault));
+      for (int k = 0; k < kSchedHdr; ++k) t.demand[p][k] = 0;
+      VX_CUDA(cudaMemsetAsync(t.buf[p] + grid + kSchedHdr, 0, (size_t)grid * 4, s));
+      t.valid[p] = false;
+    }
     t.vol = vol;
     t.w = rs->width;
     t.h = rs->height;
@@ -1840,14 +1869,14 @@ static int tile_sched(vx_volume* vol, const vx_ray_setup* rs, int rank, int worl
     t.world = world;
     t.grid = grid;
     t.stream = s;
-    t.valid = false;
+    t.parity = 0;
   }
   *out = &t;
   return VX_OK;
 }
 
-// the next frame's tile order (tile_order_kernel + the split-demand read
-// back); it only has to precede the next frame on this stream
+// the order of frame k + 2 from frame k's costs (tile_order_kernel + the
+// split-demand read back), on the side stream behind this frame's K4
 struct OrderJob {
   TileSched* ts = nullptr;
   int grid = 0;
@@ -1856,14 +1885,21 @@ struct OrderJob {
 static int order_tiles(const OrderJob& j, cudaStream_t s) {
   if (!j.ts) return VX_OK;
   TileSched* ts = j.ts;
-  tile_order_kernel<<<1, 1024, 0, s>>>(ts->buf + j.grid + kSchedHdr, ts->buf, j.grid,
-                                       g_sched_split_us.load(),
-                                       vx_sm_count() * (VX_RAYCAST_MIN_WARPS / kWarpsPerBlock));
+  const int p = ts->parity;
+  uint32_t* b = ts->buf[p];
+  VX_CUDA(cudaEventRecord(ts->costs_done[p], s));
+  VX_CUDA(cudaStreamWaitEvent(ts->side, ts->costs_done[p], 0));
+  tile_order_kernel<<<1, 1024, 0, ts->side>>>(b + j.grid + kSchedHdr, b, j.grid,
+                                              g_sched_split_us.load(),
+                                              vx_sm_count() * (VX_RAYCAST_MIN_WARPS / kWarpsPerBlock));
   VX_CHECK_LAUNCH();
   // the split demand, read back without a sync: it sizes a later frame's
   // reserve of extra blocks (a stale value only costs time)
-  VX_CUDA(cudaMemcpyAsync(ts->demand, ts->buf + j.grid, 4 * kSchedHdr, cudaMemcpyDeviceToHost, s));
-  ts->valid = true;
+  VX_CUDA(cudaMemcpyAsync(ts->demand[p], b + j.grid, 4 * kSchedHdr, cudaMemcpyDeviceToHost,
+                          ts->side));
+  VX_CUDA(cudaEventRecord(ts->order_done[p], ts->side));
+  ts->valid[p] = true;
+  ts->parity = p ^ 1;
   return VX_OK;
 }
 
@@ -1938,10 +1974,15 @@ static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_p
                     ? 0
                     : grid / g_sched_split_div.load();
   if (ts) {
-    a.tile_cost = ts->buf + grid + kSchedHdr;
-    a.tile_order = ts->valid ? ts->buf : nullptr;
-    if (ts->valid) {
-      const long long want = 7ll * ts->demand[0] + 3ll * ts->demand[1] + ts->demand[2];
+    const int p = ts->parity;
+    // this frame records its costs in buf[p] and renders in the order the
+    // side stream computed there from frame k - 2 (after its order is done)
+    if (ts->valid[p]) VX_CUDA(cudaStreamWaitEvent(s, ts->order_done[p], 0));
+    a.tile_cost = ts->buf[p] + grid + kSchedHdr;
+    a.tile_order = ts->valid[p] ? ts->buf[p] : nullptr;
+    if (ts->valid[p]) {
+      const uint32_t* dm = ts->demand[p];
+      const long long want = 7ll * dm[0] + 3ll * dm[1] + dm[2];
       const long long reserve = want + want / 4 + 32;
       if (reserve < a.split_max) a.split_max = (int)reserve;
     }
