@@ -43,7 +43,7 @@ for a, (s, i) in samples.items():
     agg[ln][1] += i
 ts = sum(v[0] for v in agg.values()) or 1
 ti = sum(v[1] for v in agg.values()) or 1
-src = open(src_file).read().splitlines() if src_file else []
+src = open(sys.argv[5] if len(sys.argv) > 5 else src_file).read().splitlines() if src_file else []
 for ln, (s, i) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
     text = src[ln - 1].strip()[:90] if ln and ln <= len(src) else "?"
     print(f"{ln!s:>5} stall {100*s/ts:5.1f}% inst {100*i/ti:5.1f}%  {text}")
