@@ -50,15 +50,20 @@ __global__ void brick_max_kernel(const uint8_t* __restrict__ origin, int64_t sy,
 // volume.)
 constexpr int kRowsPerBlock = 64;
 
-__global__ void __launch_bounds__(kRowsPerBlock) dist_first_x_kernel(
+// 256 threads: the 8 warps stage / store the 64 rows (one row per warp at a
+// time, lanes along x: coalesced, no per-byte index division), the first 64
+// threads sweep one row each
+__global__ void __launch_bounds__(256) dist_first_x_kernel(
     const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int mx, int64_t rows, int thr,
     int cap) {
   extern __shared__ uint8_t rowbuf[];
   const int pitch = mx | 1;  // odd pitch: threads sweeping rows hit distinct banks
   const int64_t r0 = (int64_t)blockIdx.x * kRowsPerBlock;
   const int nr = (int)min((int64_t)kRowsPerBlock, rows - r0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint8_t* s = src + r0 * mx;
-  for (int i = threadIdx.x; i < nr * mx; i += blockDim.x) rowbuf[(i / mx) * pitch + i % mx] = s[i];
+  for (int r = warp; r < nr; r += 8)
+    for (int x = lane; x < mx; x += 32) rowbuf[r * pitch + x] = s[(int64_t)r * mx + x];
   __syncthreads();
   if ((int)threadIdx.x < nr) {
     uint8_t* L = rowbuf + threadIdx.x * pitch;
@@ -75,7 +80,8 @@ __global__ void __launch_bounds__(kRowsPerBlock) dist_first_x_kernel(
   }
   __syncthreads();
   uint8_t* d = dst + r0 * mx;
-  for (int i = threadIdx.x; i < nr * mx; i += blockDim.x) d[i] = rowbuf[(i / mx) * pitch + i % mx];
+  for (int r = warp; r < nr; r += 8)
+    for (int x = lane; x < mx; x += 32) d[(int64_t)r * mx + x] = rowbuf[r * pitch + x];
 }
 
 // Passes 2-3 as two linear sweeps per line.  Left sweep: L(l) = min over
@@ -87,51 +93,65 @@ __global__ void __launch_bounds__(kRowsPerBlock) dist_first_x_kernel(
 // (l - last[m] <= m; only w = m can keep the value m), else m + 1 -- then
 // min with v(l).  One lookup of last[m] per step, O(n) per line (the outward
 // scan of the former kernel was O(cap) per cell: 0.15-0.53 ms per pass at
-// 1024^3).  The right sweep mirrors it; D = min(L, R), capped.  Each thread
-// owns one line (an x-column); the block stages 64 columns in shared memory.
+// 1024^3).  The right sweep mirrors it; D = min(L, R), capped.  A block
+// stages 64 x-columns (lines) in shared memory with all 256 threads; 64 of
+// them then sweep one line each.
 constexpr int kSweepCols = 64;
 
 template <int AXIS>
-__global__ void __launch_bounds__(kSweepCols) dist_sweep_kernel(const uint8_t* __restrict__ src,
-                                                               uint8_t* __restrict__ dst, int mx,
-                                                               int my, int mz, int cap) {
+__global__ void __launch_bounds__(4 * kSweepCols) dist_sweep_kernel(const uint8_t* __restrict__ src,
+                                                                   uint8_t* __restrict__ dst,
+                                                                   int mx, int my, int mz, int cap) {
   extern __shared__ uint8_t sweep_sm[];
   const int n = AXIS == 1 ? my : mz;
-  const int tx = threadIdx.x;
   uint8_t* val = sweep_sm;                                   // [n][64] v, then D
   uint8_t* left = sweep_sm + (size_t)n * kSweepCols;         // [n][64] L
   uint16_t* last = reinterpret_cast<uint16_t*>(sweep_sm + (size_t)2 * n * kSweepCols);  // [32][64]
-  const int x = blockIdx.x * kSweepCols + tx;
-  if (x >= mx) return;  // columns are independent: no block-wide barrier below
   const int64_t stride = AXIS == 1 ? (int64_t)mx : (int64_t)mx * my;
-  const int64_t base = AXIS == 1 ? (int64_t)blockIdx.y * mx * my + x : (int64_t)blockIdx.y * mx + x;
-  for (int l = 0; l < n; ++l) val[l * kSweepCols + tx] = src[base + l * stride];
-  constexpr uint16_t kNone = 0xffffu;
-  // left sweep
-  for (int w = 0; w < 32; ++w) last[w * kSweepCols + tx] = kNone;
-  int m = cap;
-  for (int l = 0; l < n; ++l) {
-    const int v = val[l * kSweepCols + tx];
-    if (v < cap) last[v * kSweepCols + tx] = (uint16_t)l;
-    if (m < cap) {
-      const int lm = last[m * kSweepCols + tx];
-      if (lm == kNone || l - lm > m) m = min(m + 1, cap);
-    }
-    if (v < m) m = v;
-    left[l * kSweepCols + tx] = (uint8_t)m;
+  const int64_t base0 = AXIS == 1 ? (int64_t)blockIdx.y * mx * my : (int64_t)blockIdx.y * mx;
+  const int x0 = blockIdx.x * kSweepCols;
+  // staging by all 256 threads: 4 lines' rows at a time, lanes along x
+  {
+    const int c = threadIdx.x & (kSweepCols - 1), r = threadIdx.x / kSweepCols;
+    if (x0 + c < mx)
+      for (int l = r; l < n; l += 4) val[l * kSweepCols + c] = src[base0 + l * stride + x0 + c];
   }
-  // right sweep, then D = min(L, R) in place of v
-  for (int w = 0; w < 32; ++w) last[w * kSweepCols + tx] = kNone;
-  m = cap;
-  for (int l = n - 1; l >= 0; --l) {
-    const int v = val[l * kSweepCols + tx];
-    if (v < cap) last[v * kSweepCols + tx] = (uint16_t)l;
-    if (m < cap) {
-      const int lm = last[m * kSweepCols + tx];
-      if (lm == kNone || lm - l > m) m = min(m + 1, cap);
+  __syncthreads();
+  const int tx = threadIdx.x;
+  if (tx < kSweepCols && x0 + tx < mx) {
+    constexpr uint16_t kNone = 0xffffu;
+    // left sweep
+    for (int w = 0; w < 32; ++w) last[w * kSweepCols + tx] = kNone;
+    int m = cap;
+    for (int l = 0; l < n; ++l) {
+      const int v = val[l * kSweepCols + tx];
+      if (v < cap) last[v * kSweepCols + tx] = (uint16_t)l;
+      if (m < cap) {
+        const int lm = last[m * kSweepCols + tx];
+        if (lm == kNone || l - lm > m) m = min(m + 1, cap);
+      }
+      if (v < m) m = v;
+      left[l * kSweepCols + tx] = (uint8_t)m;
     }
-    if (v < m) m = v;
-    dst[base + l * stride] = (uint8_t)min(m, (int)left[l * kSweepCols + tx]);
+    // right sweep, then D = min(L, R) in place of v (v(l) is not read again)
+    for (int w = 0; w < 32; ++w) last[w * kSweepCols + tx] = kNone;
+    m = cap;
+    for (int l = n - 1; l >= 0; --l) {
+      const int v = val[l * kSweepCols + tx];
+      if (v < cap) last[v * kSweepCols + tx] = (uint16_t)l;
+      if (m < cap) {
+        const int lm = last[m * kSweepCols + tx];
+        if (lm == kNone || lm - l > m) m = min(m + 1, cap);
+      }
+      if (v < m) m = v;
+      val[l * kSweepCols + tx] = (uint8_t)min(m, (int)left[l * kSweepCols + tx]);
+    }
+  }
+  __syncthreads();
+  {
+    const int c = threadIdx.x & (kSweepCols - 1), r = threadIdx.x / kSweepCols;
+    if (x0 + c < mx)
+      for (int l = r; l < n; l += 4) dst[base0 + l * stride + x0 + c] = val[l * kSweepCols + c];
   }
 }
 
@@ -258,8 +278,8 @@ static int dist_transform(const uint8_t* maxmap, uint8_t* out, int mx, int my, i
   const size_t s0 = (size_t)kRowsPerBlock * (mx | 1);
   int rc = smem_opt_in((const void*)dist_first_x_kernel, s0);
   if (rc) return rc;
-  dist_first_x_kernel<<<(unsigned)((rows + kRowsPerBlock - 1) / kRowsPerBlock), kRowsPerBlock, s0,
-                        s>>>(maxmap, out, mx, rows, thr, cap);
+  dist_first_x_kernel<<<(unsigned)((rows + kRowsPerBlock - 1) / kRowsPerBlock), 256, s0, s>>>(
+      maxmap, out, mx, rows, thr, cap);
   VX_CHECK_LAUNCH();
   const unsigned gx = (unsigned)((mx + kSweepCols - 1) / kSweepCols);
   // values >= cap never enter last[32]: the caps in use are 24 and 32
@@ -270,10 +290,12 @@ static int dist_transform(const uint8_t* maxmap, uint8_t* out, int mx, int my, i
   auto sweep_smem = [](int n) { return (size_t)2 * n * kSweepCols + 64 * kSweepCols; };
   const size_t s1 = sweep_smem(my), s2 = sweep_smem(mz);
   if ((rc = smem_opt_in((const void*)dist_sweep_kernel<1>, s1))) return rc;
-  dist_sweep_kernel<1><<<dim3(gx, (unsigned)mz), kSweepCols, s1, s>>>(out, tmp, mx, my, mz, cap);
+  dist_sweep_kernel<1><<<dim3(gx, (unsigned)mz), 4 * kSweepCols, s1, s>>>(out, tmp, mx, my, mz,
+                                                                             cap);
   VX_CHECK_LAUNCH();
   if ((rc = smem_opt_in((const void*)dist_sweep_kernel<2>, s2))) return rc;
-  dist_sweep_kernel<2><<<dim3(gx, (unsigned)my), kSweepCols, s2, s>>>(tmp, out, mx, my, mz, cap);
+  dist_sweep_kernel<2><<<dim3(gx, (unsigned)my), 4 * kSweepCols, s2, s>>>(tmp, out, mx, my, mz,
+                                                                             cap);
   VX_CHECK_LAUNCH();
   VX_CUDA(cudaFreeAsync(tmp, s));
   return VX_OK;

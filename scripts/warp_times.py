@@ -24,7 +24,7 @@ object.__setattr__(v, "_content_hash", "x")
 cam = vx.orbit_camera(v)
 p = vx.RenderParams(width=W, height=W)
 cfg = vx.FilterConfig(kind=vx.FilterKind.from_name(kind)).resolve_threshold(h)
-for _ in range(4):
+for _ in range(10):  # the schedule (order from frame k-2's costs) converges over a few frames
     d = render_detail(v, cam, p, cfg, h, diagnostics=True)
 nmax = 2 * W * W // 32
 lib = _lib.load()
@@ -35,7 +35,11 @@ dg = np.zeros(nmax * 9, np.uint32)
 lib.vx_debug_warp_diag(C.c_void_p(dg.ctypes.data), nmax)
 dg = dg.reshape(nmax, 9)
 # warps of this frame only (spare blocks of the reserve leave no record)
-keep = (t0 > 0) & (t0.astype(np.float64) >= float(t0.max()) - 5e6)
+# records of earlier frames (slots this launch did not use) end before this
+# frame's first warp: keep everything after the largest start gap
+ts = np.sort(t0[t0 > 0].astype(np.float64))
+cut = ts[np.argmax(np.diff(ts)) + 1] if len(ts) > 1 and np.diff(ts).max() > 20e3 else ts[0]
+keep = (t0 > 0) & (t0.astype(np.float64) >= cut)
 idx = np.nonzero(keep)[0]
 t0, t1, info, dg = t0[keep], t1[keep], info[keep], dg[keep]
 sm, nseg, part, tile = info & 0xff, (info >> 8) & 0xf, (info >> 12) & 0xf, info >> 16
