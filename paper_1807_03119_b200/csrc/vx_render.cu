@@ -2142,9 +2142,27 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
   const size_t o_val = out->hit_value ? take(npx * 8) : 0;
   const size_t o_int = out->intensity ? take(npx * 8) : 0;
   const size_t o_small = take(256 * 8 + 3 * 8 + 8 + 64);
-  Scratch sc(s);
-  VX_CUDA(vx_malloc_async(reinterpret_cast<uint8_t**>(&sc.p), off, s));
-  uint8_t* base = sc.get<uint8_t>();
+  // per-thread staging, kept between frames (this call synchronises before
+  // returning, so the next frame on this thread may reuse it)
+  static thread_local struct Staging {
+    uint8_t* p = nullptr;
+    size_t cap = 0;
+    int dev = -1;
+    cudaStream_t s = nullptr;
+  } st;
+  {
+    int dev = 0;
+    VX_CUDA(cudaGetDevice(&dev));
+    if (!st.p || st.cap < off || st.dev != dev || st.s != s) {
+      if (st.p && st.dev == dev) VX_CUDA(cudaFreeAsync(st.p, st.s));
+      st.p = nullptr;
+      VX_CUDA(vx_malloc_async(&st.p, off, s));
+      st.cap = off;
+      st.dev = dev;
+      st.s = s;
+    }
+  }
+  uint8_t* base = st.p;
   VX_CUDA(cudaMemsetAsync(base + o_small, 0, 256 * 8 + 3 * 8 + 8 + 64, s));
   if (part && part->world > 1) VX_CUDA(cudaMemsetAsync(base + o_pix, 0, npx, s));
   VX_TRACE("staging", tv);

@@ -347,8 +347,22 @@ class FrameDetail:
     device_ms: float | None = None  # CUDA-event K4 time (frame_timing() on)
 
 
+_resolved: dict = {}  # (id(config), id(histogram)) -> (config, histogram, resolved)
+
+
 def _check_render_args(config: FilterConfig, histogram, filter_fn) -> FilterConfig:
-    config = config.resolve_threshold(histogram)
+    if config.threshold is None:
+        # an auto-threshold config resolves to the same FilterConfig every
+        # frame: reuse it (the struct caches below key on its identity)
+        hit = _resolved.get((id(config), id(histogram)))
+        if hit is not None and hit[0] is config and hit[1] is histogram:
+            config = hit[2]
+        else:
+            resolved = config.resolve_threshold(histogram)
+            if len(_resolved) > 64:
+                _resolved.clear()
+            _resolved[(id(config), id(histogram))] = (config, histogram, resolved)
+            config = resolved
     if config.kind in (FilterKind.SIGMA, FilterKind.ENTROPY) and histogram is None:
         raise RenderError(f"{config.kind.value} filter needs the volume histogram")
     if filter_fn is not None:
