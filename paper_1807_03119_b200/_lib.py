@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 import threading
 import weakref
 from pathlib import Path
@@ -242,6 +243,7 @@ class PinnedPool:
 
     def __init__(self):
         self._free: dict[int, list[int]] = {}
+        self._frames: dict[tuple[int, int], list[list]] = {}
         self._lock = threading.Lock()
 
     def array(self, shape, dtype) -> np.ndarray:
@@ -273,6 +275,42 @@ class PinnedPool:
     def _release(self, nbytes, ptr):
         with self._lock:
             self._free.setdefault(nbytes, []).append(ptr)
+
+    def frame(self, height: int, width: int) -> tuple[np.ndarray, np.ndarray, int, int]:
+        """(pixels (H, W) uint8, counters int64[266], pixels address, counters
+        address) in one page-locked buffer, recycled without per-frame ctypes
+        or finalizer work: an entry is free again when nothing outside the pool
+        references its arrays (views such as ``counters[:256]`` hold a
+        reference too)."""
+        key = (height, width)
+        with self._lock:
+            lst = self._frames.setdefault(key, [])
+            for ent in lst:
+                # free when only the entry references its arrays and its
+                # buffer: numpy views of views may point at either the view or
+                # the buffer object (base collapsing), so both are counted
+                if (sys.getrefcount(ent[0]) == 2 and sys.getrefcount(ent[1]) == 2
+                        and sys.getrefcount(ent[4]) == ent[5]
+                        and sys.getrefcount(ent[6]) == ent[7]):
+                    pix, small = ent[0], ent[1]  # held before the lock is released
+                    return pix, small, ent[2], ent[3]
+            n_new = 1 if lst else 2  # a spare for double buffering
+        npx = height * width
+        off = (npx + 63) & ~63
+        made = []
+        for _ in range(n_new):  # allocated outside the lock (array() takes it)
+            raw = self.array((off + 266 * 8,), np.uint8)
+            ptr = raw.ctypes.data
+            ent = [raw[:npx].reshape(height, width), raw[off:].view(np.int64), ptr, ptr + off,
+                   raw.base, 0, raw, 0]
+            del raw
+            # references of the buffer object and of the flat array while unused
+            ent[5], ent[7] = sys.getrefcount(ent[4]), sys.getrefcount(ent[6])
+            made.append(ent)
+        pix, small, p0, p1 = made[0][:4]
+        with self._lock:
+            self._frames[key].extend(made)
+        return pix, small, p0, p1
 
 
 pinned = PinnedPool()

@@ -426,11 +426,9 @@ def render_detail(volume: Volume, camera: Camera, params: RenderParams, config: 
     dev = device_volume(volume)
     rs, rp, fc = _native(camera, params, config, histogram, skip)
     npx = params.width * params.height
-    # page-locked frame: the device writes it by DMA, no staging copy
-    pixels, pix_ptr = _lib.pinned.array_ptr((params.height, params.width), np.uint8)
-    # image histogram [0:256], hit count [256], samples [257], diag [258:266]
-    small = np.empty(266, dtype=np.int64)
-    sp = small.__array_interface__["data"][0]
+    # page-locked frame and counters (image histogram [0:256], hit count
+    # [256], samples [257], diag [258:266]): the device writes them by DMA
+    pixels, small, pix_ptr, sp = _lib.pinned.frame(params.height, params.width)
     out = _lib.vx_render_out()
     out.pixels = pix_ptr
     out.image_hist = sp

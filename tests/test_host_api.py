@@ -197,3 +197,44 @@ def test_frame_header_layout_matches_reference():
     assert h == {"magic": b"VXSF", "version": 1, "sequence": 3, "width": 640, "height": 480,
                  "render_ms": 1.5, "digest": b"ABCDEFGH"}
     assert m[32:] == b"\x01\x02"
+
+
+def test_pinned_frame_pool_recycles_only_unreferenced_buffers(monkeypatch):
+    """The frame pool hands a page-locked buffer out again only when no array
+    or view of it is alive (views of views may reference the flat array or
+    the buffer object); double buffering never allocates after warm-up."""
+    import ctypes as C
+
+    from paper_1807_03119_b200 import _lib
+
+    keep = []
+    allocs = []
+
+    def fake_call(name, *args, **kw):
+        assert name == "vx_host_alloc"
+        b = (C.c_uint8 * args[0])()
+        keep.append(b)
+        allocs.append(args[0])
+        args[1]._obj.value = C.addressof(b)
+
+    monkeypatch.setattr(_lib, "call", fake_call)
+    pool = _lib.PinnedPool()
+    for trial in range(4):
+        pix, small, p0, p1 = pool.frame(6, 10)
+        assert pix.shape == (6, 10) and small.shape == (266,) and p1 - p0 >= 60
+        held = [small[:256], pix[1:3], pix.reshape(-1)[2:5], small[256:257].view(np.uint8)][trial]
+        del pix, small
+        handed = set()
+        for _ in range(5):
+            q = pool.frame(6, 10)
+            handed.add(q[2])
+            del q
+        assert p0 not in handed
+        del held
+    n = len(allocs)
+    prev = pool.frame(6, 10)
+    for _ in range(10):  # render k+1 while frame k is still held
+        cur = pool.frame(6, 10)
+        assert cur[2] != prev[2]
+        prev = cur
+    assert len(allocs) == n
