@@ -2141,6 +2141,16 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
   const size_t o_t = out->hit_t ? take(npx * 4) : 0;
   const size_t o_val = out->hit_value ? take(npx * 8) : 0;
   const size_t o_int = out->intensity ? take(npx * 8) : 0;
+  // the Python frame pool lays the counters out right behind the pixels (at
+  // npx rounded to 64 B) in the same page-locked buffer: then one copy brings
+  // pixels and counters back (saves a copy's fixed latency per frame)
+  const size_t o_fused = (npx + 63) & ~size_t(63);
+  const bool fused = !out->hit_voxel && !out->hit_t && !out->hit_value && !out->intensity &&
+                     !out->diag && out->image_hist &&
+                     reinterpret_cast<uint8_t*>(out->image_hist) == out->pixels + o_fused &&
+                     out->hit_count == out->image_hist + 256 &&
+                     out->samples == out->image_hist + 257;
+  if (fused) off = o_fused;
   const size_t o_small = take(256 * 8 + 3 * 8 + 8 + 64);
   // per-thread staging, kept between frames (this call synchronises before
   // returning, so the next frame on this thread may reuse it)
@@ -2199,8 +2209,12 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
   cudaEvent_t copied = nullptr;
   VX_CUDA(copy_event(&copied));
   auto copy_back = [&]() -> int {
-    VX_CUDA(cudaMemcpyAsync(out->pixels, d.pixels, npx, cudaMemcpyDeviceToHost, s));
-    VX_CUDA(cudaMemcpyAsync(small_h, small, sizeof(small_h), cudaMemcpyDeviceToHost, s));
+    if (fused) {  // pixels, padding, histogram, hit count, samples, flag
+      VX_CUDA(cudaMemcpyAsync(out->pixels, d.pixels, o_fused + 259 * 8, cudaMemcpyDeviceToHost, s));
+    } else {
+      VX_CUDA(cudaMemcpyAsync(out->pixels, d.pixels, npx, cudaMemcpyDeviceToHost, s));
+      VX_CUDA(cudaMemcpyAsync(small_h, small, sizeof(small_h), cudaMemcpyDeviceToHost, s));
+    }
     if (out->hit_voxel)
       VX_CUDA(cudaMemcpyAsync(out->hit_voxel, d.hit_voxel, npx * 12, cudaMemcpyDeviceToHost, s));
     if (out->hit_t) VX_CUDA(cudaMemcpyAsync(out->hit_t, d.hit_t, npx * 4, cudaMemcpyDeviceToHost, s));
@@ -2213,6 +2227,7 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
     order = OrderJob();
     if (r2) return r2;
     VX_CUDA(cudaEventSynchronize(copied));
+    if (fused) memcpy(small_h, out->image_hist, 259 * 8);
     return VX_OK;
   };
   double tc = trace_on() ? trace_us() : 0.0;
@@ -2239,9 +2254,11 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
     ms += ms2;
   }
   tl_render_ms = timed ? ms : -1.0f;
-  if (out->image_hist) memcpy(out->image_hist, small_h, 256 * 8);
-  if (out->hit_count) out->hit_count[0] = small_h[256];
-  if (out->samples) out->samples[0] = small_h[257];
+  if (!fused) {
+    if (out->image_hist) memcpy(out->image_hist, small_h, 256 * 8);
+    if (out->hit_count) out->hit_count[0] = small_h[256];
+    if (out->samples) out->samples[0] = small_h[257];
+  }
   if (out->diag) memcpy(out->diag, small_h + 259, 8 * 8);
   if (out->trunc_flag) out->trunc_flag[0] = 0;
   return VX_OK;
