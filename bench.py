@@ -454,8 +454,12 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "raycast_kernel<LOCAL_CLUSTER>", "kernel_ms": kms,
                          "alg_bytes": alg_bytes, "peak_source": peak_kind,
+                         "dram_achieved": (traffic / (kms * 1e-3) / 1e9) if traffic else None,
+                         "dram_frac": (traffic / (kms * 1e-3) / 1e9 / peak) if traffic else None,
                          "note": "effective: exact empty-space skipping reads far less than the "
-                                 "volume; traffic = ncu dram bytes per launch"},
+                                 "volume (frac > 1 = faster than reading it once); traffic = ncu "
+                                 "dram bytes per launch, dram_frac = that traffic's share of the "
+                                 "peak (the kernel is latency/issue-bound, not HBM-bound)"},
             "otsu_hist": hist_line,
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
@@ -463,9 +467,11 @@ def run_ours(args):
                       "kernel_ms_median": statistics.median(kern_ms),
                       "step_ms_median": statistics.median(step_ms),
                       "cold_ms": cold_ms,
-                      "cold_note": "wall ms of warm-up frames 1-2: frame 1 builds the candidate "
-                                   "distance map of thr, frame 2 the filter's accepted-cell "
-                                   "map; timed frames reuse both (per volume/setting caches)"},
+                      "cold_note": "wall ms of warm-up frames 1-2: frame 1 renders on the "
+                                   "candidate distance map (built with the volume) and schedules "
+                                   "its first tile order, frame 2 builds the filter's "
+                                   "accepted-cell map; timed frames reuse both (per "
+                                   "volume/setting caches)"},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
