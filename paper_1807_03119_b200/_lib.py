@@ -241,10 +241,39 @@ class PinnedPool:
     the numpy arrays the caller receives; cudaHostAlloc is too slow per frame).
     A buffer returns to the pool when the last array viewing it is freed."""
 
+    ARENA_BYTES = 16 << 20  # two 2048^2 frames with counters, or many smaller ones
+
     def __init__(self):
         self._free: dict[int, list[int]] = {}
         self._frames: dict[tuple[int, int], list[list]] = {}
         self._lock = threading.Lock()
+        self._arena = 0  # page-locked block new buffers are carved from
+        self._arena_left = 0
+
+    def prewarm(self) -> None:
+        """Allocate the page-locked arena now (called when a device volume is
+        created): the first frame then carves its buffers instead of paying
+        cudaHostAlloc, whose cost (1-25 ms measured) depends on the host."""
+        with self._lock:
+            if self._arena:
+                return
+        p = C.c_void_p()
+        call("vx_host_alloc", self.ARENA_BYTES, C.byref(p))
+        with self._lock:
+            if self._arena:  # another thread won: keep theirs, park ours as a buffer
+                self._free.setdefault(self.ARENA_BYTES, []).append(p.value)
+                return
+            self._arena, self._arena_left = p.value, self.ARENA_BYTES
+
+    def _carve(self, nbytes: int) -> int | None:
+        """A fresh buffer from the arena (256-byte aligned), or None."""
+        need = (max(nbytes, 1) + 255) & ~255
+        with self._lock:
+            if not self._arena or need > self._arena_left:
+                return None
+            ptr = self._arena + (self.ARENA_BYTES - self._arena_left)
+            self._arena_left -= need
+            return ptr
 
     def array(self, shape, dtype) -> np.ndarray:
         return self.array_ptr(shape, dtype)[0]
@@ -259,6 +288,8 @@ class PinnedPool:
         with self._lock:
             lst = self._free.get(nbytes)
             ptr = lst.pop() if lst else None
+        if ptr is None:
+            ptr = self._carve(nbytes)
         if ptr is None:
             # a miss allocates a spare too: a caller that keeps the previous
             # frame while rendering the next (double buffering) then never

@@ -177,7 +177,7 @@ int vx_volume_alloc(int64_t nx, int64_t ny, int64_t nz, vx_volume** out) {
     return vx_cuda_fail(e, "cudaMalloc(volume)", __FILE__, __LINE__);
   }
   const uint64_t slot = v->map_bytes + v->cmap_bytes;
-  e = cudaMalloc(&v->bmax, slot * (1 + VX_DIST_CACHE + VX_ACC_CACHE));
+  e = cudaMalloc(&v->bmax, slot * (1 + VX_DIST_CACHE + VX_ACC_CACHE) + 2 * v->cmap_bytes);
   if (e != cudaSuccess) {
     cudaFree(v->alloc);
     delete v;
@@ -186,6 +186,7 @@ int vx_volume_alloc(int64_t nx, int64_t ny, int64_t nz, vx_volume** out) {
   v->cmax = v->bmax + v->map_bytes;
   for (int i = 0; i < VX_DIST_CACHE; ++i) v->dist[i].map = v->bmax + slot * (1 + i);
   for (int i = 0; i < VX_ACC_CACHE; ++i) v->acc[i].map = v->bmax + slot * (1 + VX_DIST_CACHE + i);
+  v->scratch = v->bmax + slot * (1 + VX_DIST_CACHE + VX_ACC_CACHE);
   v->origin = v->alloc + VX_PAD * v->sz + VX_PAD * v->sy + VX_PAD;
   *out = v;
   return VX_OK;
@@ -232,6 +233,11 @@ int vx_volume_finish(vx_volume* v, const uint8_t* compact_dev, cudaStream_t s) {
     const uint8_t* m = nullptr;
     if (T > 0 && T <= 255 && (rc = vx_get_dist_map(v, T, &m, s))) return rc;
     if ((rc = vx_preload_render_kernels())) return rc;
+    // grow the stream-ordered pool once (it keeps freed memory: release
+    // threshold above), so a first frame's staging comes from retained memory
+    uint8_t* warm = nullptr;
+    VX_CUDA(vx_malloc_async(&warm, 64ull << 20, s));
+    VX_CUDA(cudaFreeAsync(warm, s));
   }
   return VX_OK;
 }

@@ -100,6 +100,9 @@ struct vx_volume {
   uint64_t cmap_bytes;
   DistEntry dist[VX_DIST_CACHE];
   AccEntry acc[VX_ACC_CACHE];
+  // two cell-map-sized scratch regions for the map builds (occupancy and the
+  // distance passes' intermediate), used under `mu`
+  uint8_t* scratch;
   uint64_t stamp;
   uint64_t counts[256];
   std::mutex mu;
@@ -118,6 +121,7 @@ int vx_launch_hist_otsu(const uint8_t* dev, uint64_t n, uint64_t* dev_counts, in
 int vx_launch_entropy(const uint64_t* dev_counts, uint64_t n, double* dev_H, cudaStream_t s);
 int vx_launch_brick_max(vx_volume* v, cudaStream_t s);
 int vx_launch_dist_map(const vx_volume* v, int thr, uint8_t* map, cudaStream_t s);
+// (callers hold v->mu: the builds use v->scratch)
 int vx_launch_cell_max(vx_volume* v, cudaStream_t s);
 // Chebyshev cell-distance map (cap VX_FINE_CAP) of the cells whose value in
 // `occ` (cell-map layout, apron included) is >= thr

@@ -1733,8 +1733,7 @@ static int get_accept_map(vx_volume* v, const RenderArgs& a, bool checked, const
   }
   double tt = trace_on() ? trace_us() : 0.0;
   e->valid = false;  // until built
-  uint8_t* occ = nullptr;
-  VX_CUDA(vx_malloc_async(&occ, v->cmap_bytes, s));
+  uint8_t* occ = v->scratch;  // the volume's build scratch (held under v->mu)
   VX_CUDA(cudaMemsetAsync(occ, 0, v->cmap_bytes, s));
   VX_CUDA(cudaMemsetAsync(e->map, 0, v->map_bytes, s));  // coarse level unused: no skip
   VX_TRACE("  acc scratch", tt);
@@ -1759,7 +1758,6 @@ static int get_accept_map(vx_volume* v, const RenderArgs& a, bool checked, const
   VX_CHECK_LAUNCH();
   int rc = vx_launch_dist_cells(v, occ, e->map + v->map_bytes, 1, s);
   if (rc) return rc;
-  VX_CUDA(cudaFreeAsync(occ, s));
   VX_TRACE("  acc launches", tt);
   // other streams may pick this map up: make it visible before publishing
   VX_CUDA(cudaStreamSynchronize(s));

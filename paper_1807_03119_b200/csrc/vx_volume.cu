@@ -269,11 +269,10 @@ int vx_launch_brick_max(vx_volume* v, cudaStream_t s) {
   return VX_OK;
 }
 
+// tmp: an intermediate of mx*my*mz bytes (the volume's build scratch: a
+// stream-ordered allocation here grew the pool inside a frame, 1-20 ms)
 static int dist_transform(const uint8_t* maxmap, uint8_t* out, int mx, int my, int mz, int thr,
-                          int cap, cudaStream_t s) {
-  const int64_t n = (int64_t)mx * my * mz;
-  uint8_t* tmp = nullptr;
-  VX_CUDA(vx_malloc_async(&tmp, n, s));
+                          int cap, uint8_t* tmp, cudaStream_t s) {
   const int64_t rows = (int64_t)my * mz;
   const size_t s0 = (size_t)kRowsPerBlock * (mx | 1);
   int rc = smem_opt_in((const void*)dist_first_x_kernel, s0);
@@ -297,21 +296,22 @@ static int dist_transform(const uint8_t* maxmap, uint8_t* out, int mx, int my, i
   dist_sweep_kernel<2><<<dim3(gx, (unsigned)my), 4 * kSweepCols, s2, s>>>(tmp, out, mx, my, mz,
                                                                              cap);
   VX_CHECK_LAUNCH();
-  VX_CUDA(cudaFreeAsync(tmp, s));
   return VX_OK;
 }
 
 // coarse (bricks) then fine (cells) Chebyshev distance maps of thr into `map`
 int vx_launch_dist_map(const vx_volume* v, int thr, uint8_t* map, cudaStream_t s) {
-  int rc = dist_transform(v->bmax, map, v->nbx + 2, v->nby + 2, v->nbz + 2, thr, VX_DIST_CAP, s);
+  int rc = dist_transform(v->bmax, map, v->nbx + 2, v->nby + 2, v->nbz + 2, thr, VX_DIST_CAP,
+                          v->scratch + v->cmap_bytes, s);
   if (rc) return rc;
   return dist_transform(v->cmax, map + v->map_bytes, v->ncx + 2, v->ncy + 2, v->ncz + 2, thr,
-                        VX_FINE_CAP, s);
+                        VX_FINE_CAP, v->scratch + v->cmap_bytes, s);
 }
 
 int vx_launch_dist_cells(const vx_volume* v, const uint8_t* occ, uint8_t* out, int thr,
                          cudaStream_t s) {
-  return dist_transform(occ, out, v->ncx + 2, v->ncy + 2, v->ncz + 2, thr, VX_FINE_CAP, s);
+  return dist_transform(occ, out, v->ncx + 2, v->ncy + 2, v->ncz + 2, thr, VX_FINE_CAP,
+                        v->scratch + v->cmap_bytes, s);
 }
 
 int vx_launch_cell_max(vx_volume* v, cudaStream_t s) {

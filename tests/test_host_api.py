@@ -238,3 +238,37 @@ def test_pinned_frame_pool_recycles_only_unreferenced_buffers(monkeypatch):
         assert cur[2] != prev[2]
         prev = cur
     assert len(allocs) == n
+
+
+def test_pinned_arena_serves_first_frames(monkeypatch):
+    """After prewarm() the first frames carve their page-locked buffers from
+    the arena (no vx_host_alloc in the frame path); buffers larger than what
+    is left fall back to allocation."""
+    import ctypes as C
+
+    from paper_1807_03119_b200 import _lib
+
+    keep, allocs = [], []
+
+    def fake_call(name, *args, **kw):
+        assert name == "vx_host_alloc"
+        b = (C.c_uint8 * args[0])()
+        keep.append(b)
+        allocs.append(args[0])
+        args[1]._obj.value = C.addressof(b)
+
+    monkeypatch.setattr(_lib, "call", fake_call)
+    pool = _lib.PinnedPool()
+    pool.prewarm()
+    pool.prewarm()
+    assert allocs == [pool.ARENA_BYTES]
+    a = pool.frame(1024, 1024)
+    b = pool.frame(1024, 1024)
+    # carves are 256-byte aligned relative to the (page-aligned) arena base
+    assert len(allocs) == 1 and a[2] != b[2]
+    assert (a[2] - pool._arena) % 256 == 0 and (b[2] - pool._arena) % 256 == 0
+    # distinct, non-overlapping carves
+    lo, hi = sorted([a[2], b[2]])
+    assert hi - lo >= 1024 * 1024 + 266 * 8
+    big = pool.array((pool.ARENA_BYTES,), np.uint8)  # does not fit the rest: allocated
+    assert len(allocs) == 3 and big.size == pool.ARENA_BYTES
