@@ -124,10 +124,10 @@ static double filter_value(const Vol* V, const Filt* F, int64_t x, int64_t y, in
       for (int dx = -h; dx <= h; ++dx)
         for (int dy = -h; dy <= h; ++dy)
           for (int dz = -h; dz <= h; ++dz) terms[k++] = F->lut[vat(V, x + dx, y + dy, z + dz)];
-      double H;
+      double H = 0.0;
       if (F->pairwise) {
         H = pw_sum(terms, k);
-      } else {
+      } else if (k > 0) {
         H = terms[0];
         for (int i = 1; i < k; ++i) H += terms[i];
       }
