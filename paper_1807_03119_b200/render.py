@@ -380,17 +380,20 @@ class _StructCache:
 
         self.size = size
         self.d: OrderedDict = OrderedDict()
+        self.lock = threading.Lock()  # render_frame runs on executor threads
 
     def get(self, key, make):
         try:
-            v = self.d.pop(key)
-        except KeyError:
-            v = make()
+            with self.lock:
+                v = self.d.pop(key, None)
         except TypeError:  # unhashable key part
             return make()
-        self.d[key] = v
-        if len(self.d) > self.size:
-            self.d.popitem(last=False)
+        if v is None:
+            v = make()
+        with self.lock:
+            self.d[key] = v
+            while len(self.d) > self.size:
+                self.d.popitem(last=False)
         return v
 
 

@@ -367,3 +367,50 @@ def test_split_rays_and_tile_order_match_oracle(vx, oracle, split_everything):
                 assert np.array_equal(d.pixels, want["pixels"]), (trial, kind, T, rep)
                 if rep == 2:
                     assert np.array_equal(d.hit_voxel, want["hit_voxel"]), (trial, kind, T)
+
+
+def test_concurrent_render_frame_threads(vx):
+    """The reference service renders from executor threads on one shared
+    volume (service.py:234-236): four threads, each with its own cameras and
+    filter settings, give the same frames as a single-threaded render."""
+    import threading
+
+    from paper_1807_03119_b200 import phantoms
+    from oracle.rng_np import generate_phantom_np
+
+    spec = phantoms.spot_phantom_spec(64)
+    v = vx.Volume(dims=spec.dims, data=generate_phantom_np(spec.to_json()))
+    h = vx.build_histogram(v)
+    kinds = [vx.FilterKind.LOCAL_CLUSTER, vx.FilterKind.MEAN, vx.FilterKind.NONE,
+             vx.FilterKind.ENTROPY]
+    jobs = []
+    for w in range(4):
+        for r in range(3):
+            cam = vx.orbit_camera(v, azimuth_deg=30.0 * w + 11.0 * r, elevation_deg=10.0 + 7 * r)
+            cfg = vx.FilterConfig(kind=kinds[(w + r) % 4])
+            jobs.append((w, cam, cfg))
+    # 320x300 = 760 tiles: above the scheduler's threshold, so each thread's
+    # cost-ordered tiles, split rays and side-stream ordering are exercised
+    params = vx.RenderParams(width=320, height=300)
+    want = {i: vx.render_frame(v, cam, params, cfg, h).pixels.copy()
+            for i, (_, cam, cfg) in enumerate(jobs)}
+    got, errors = {}, []
+
+    def worker(w):
+        try:
+            for rep in range(4):
+                for i, (ww, cam, cfg) in enumerate(jobs):
+                    if ww == w:
+                        got[(i, rep)] = vx.render_frame(v, cam, params, cfg, h).pixels.copy()
+        except Exception as exc:  # surfaced below
+            errors.append(exc)
+
+    ts = [threading.Thread(target=worker, args=(w,)) for w in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    for (i, rep), px in got.items():
+        assert np.array_equal(px, want[i]), (i, rep)
+    assert len(got) == len(jobs) * 4
