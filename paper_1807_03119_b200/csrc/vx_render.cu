@@ -61,6 +61,13 @@ constexpr bool kSplitRays = VX_SPLIT_RAYS && kWarpsPerBlock == 4;
 
 // sample-group passes whose loads are issued together (2 or 4; 0 = per
 // filter kind, see march())
+#ifndef VX_COOP_FIRST
+// local cluster: when at most this many lanes of a warp evaluate a first
+// candidate, the whole warp splits each one's taps (0 = owner lanes only).
+// Measured (bench frame / C2 / C4): 2 -> -3 % / 0 / +0.8 %; 4 -> -3 % /
+// +0.9 % / +1.3 %; 8 and 32 slower; two candidates per trip slower
+#define VX_COOP_FIRST 2
+#endif
 #ifndef VX_GROUP_PIPE
 #define VX_GROUP_PIPE 0
 #endif
@@ -310,6 +317,38 @@ __device__ double filter_axis(const VolView& V, const FiltD& F, long long x, lon
   for (int i = -h; i <= h; ++i)
     sum += rd<CHECKED>(V, x + i, y, z) + rd<CHECKED>(V, x, y + i, z) + rd<CHECKED>(V, x, y, z + i);
   return __ddiv_rn((double)sum, (double)(3 * F.M));
+}
+
+// This lane's share of filter_lc's integer sum at (x, y, z): the 9 clusters'
+// 3M-2 distinct taps each (centre weighted 3: the three arms share it),
+// dealt round-robin over the warp.  Integer sums are order-free, so the warp
+// total equals filter_lc's sum exactly.
+template <bool CHECKED>
+__device__ __forceinline__ int lc_tap_share(const VolView& V, const FiltD& F, int x, int y,
+                                            int z, unsigned lane) {
+  const int M = F.M, h = (M - 1) >> 1;
+  const int P = 3 * M - 2, T = 9 * P;
+  int s = 0;
+  for (int t = (int)lane; t < T; t += 32) {
+    const int c = (M == 3) ? t / 7 : t / P;
+    const int r = t - c * P;
+    int cx = x, cy = y, cz = z;
+    if (c > 0) {
+      const int q = c - 1;
+      cx += ((q >> 2) & 1 ? F.d : -F.d);
+      cy += ((q >> 1) & 1 ? F.d : -F.d);
+      cz += (q & 1 ? F.d : -F.d);
+    }
+    if (r == 0) {
+      s += 3 * rd<CHECKED>(V, cx, cy, cz);
+    } else {
+      const int a = (M == 3) ? (r - 1) >> 1 : (r - 1) / (M - 1);
+      const int idx = (r - 1) - a * (M - 1);
+      const int i = idx < h ? idx - h : idx - h + 1;
+      s += rd<CHECKED>(V, cx + (a == 0 ? i : 0), cy + (a == 1 ? i : 0), cz + (a == 2 ? i : 0));
+    }
+  }
+  return s;
 }
 
 constexpr int kAxisCluster = 6;  // K5-only kind
@@ -745,7 +784,51 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
         nsamp += __popc(my_v);
       }
       unsigned rem = 0;
-      if (need && my_c) {
+      bool coop = false;
+      if (VX_COOP_FIRST && KIND == VX_FILTER_LOCAL_CLUSTER) {
+        const unsigned fm = __ballot_sync(0xffffffffu, need && my_c);
+        coop = fm != 0 && __popc(fm) <= VX_COOP_FIRST;
+        if (coop) {
+          int cx = 0, cy = 0, cz = 0;
+          const int j = my_c ? __ffs(my_c) - 1 : 0;
+          if (need && my_c) {
+            const float t = sample_t(base, M.s, k + j);
+            float px = pos1(R.o[0], t, R.d[0]);
+            float py = pos1(R.o[1], t, R.d[1]);
+            float pz = pos1(R.o[2], t, R.d[2]);
+            if (M.need_clip) {
+              px = clip1(px, M.xmax);
+              py = clip1(py, M.ymax);
+              pz = clip1(pz, M.zmax);
+            }
+            cx = __float2int_rz(px);
+            cy = __float2int_rz(py);
+            cz = __float2int_rz(pz);
+          }
+          unsigned c = fm;
+          while (c) {
+            const int src = __ffs(c) - 1;
+            c &= c - 1;
+            const int sx = __shfl_sync(0xffffffffu, cx, src);
+            const int sy = __shfl_sync(0xffffffffu, cy, src);
+            const int sz = __shfl_sync(0xffffffffu, cz, src);
+            const int sum =
+                __reduce_add_sync(0xffffffffu, lc_tap_share<CHECKED>(V, F, sx, sy, sz, lane));
+            if ((int)lane == src) {
+              VX_DIAG(dFilter);
+              if (__ddiv_rn((double)sum, (double)(27 * F.M)) >= M.T) {
+                VX_DIAG(dHit);
+                ht = sample_t(base, M.s, k + j);
+                k += j;
+                status = kHit;
+              } else {
+                rem = my_c & (my_c - 1);
+              }
+            }
+          }
+        }
+      }
+      if (!coop && need && my_c) {
         const int j = __ffs(my_c) - 1;
         const float t = sample_t(base, M.s, k + j);
         float px = pos1(R.o[0], t, R.d[0]);
