@@ -68,6 +68,11 @@ constexpr bool kSplitRays = VX_SPLIT_RAYS && kWarpsPerBlock == 4;
 // +0.9 % / +1.3 %; 8 and 32 slower; two candidates per trip slower
 #define VX_COOP_FIRST 2
 #endif
+#ifndef VX_COOP_MEAN
+// the same for the box mean: 4 -> C1 mean -4.5 %, C2 mean 0 (2: +1.6 % on
+// C2, 32: +3 %)
+#define VX_COOP_MEAN 4
+#endif
 #ifndef VX_GROUP_PIPE
 #define VX_GROUP_PIPE 0
 #endif
@@ -347,6 +352,23 @@ __device__ __forceinline__ int lc_tap_share(const VolView& V, const FiltD& F, in
       const int i = idx < h ? idx - h : idx - h + 1;
       s += rd<CHECKED>(V, cx + (a == 0 ? i : 0), cy + (a == 1 ? i : 0), cz + (a == 2 ? i : 0));
     }
+  }
+  return s;
+}
+
+// This lane's share of filter_mean's integer sum (the M^3 box), dealt
+// round-robin over the warp.
+template <bool CHECKED>
+__device__ __forceinline__ int mean_tap_share(const VolView& V, const FiltD& F, int x, int y,
+                                              int z, unsigned lane) {
+  const int M = F.M, h = (M - 1) >> 1;
+  int s = 0;
+  for (int t = (int)lane; t < M * M * M; t += 32) {
+    const int dz = (M == 3) ? t / 9 : t / (M * M);
+    const int r = t - dz * M * M;
+    const int dy = (M == 3) ? r / 3 : r / M;
+    const int dx = r - dy * M;
+    s += rd<CHECKED>(V, x + dx - h, y + dy - h, z + dz - h);
   }
   return s;
 }
@@ -785,9 +807,11 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
       }
       unsigned rem = 0;
       bool coop = false;
-      if (VX_COOP_FIRST && KIND == VX_FILTER_LOCAL_CLUSTER) {
+      constexpr int kCoop = KIND == VX_FILTER_LOCAL_CLUSTER ? VX_COOP_FIRST
+                            : (KIND == VX_FILTER_MEAN ? VX_COOP_MEAN : 0);
+      if (kCoop) {
         const unsigned fm = __ballot_sync(0xffffffffu, need && my_c);
-        coop = fm != 0 && __popc(fm) <= VX_COOP_FIRST;
+        coop = fm != 0 && __popc(fm) <= kCoop;
         if (coop) {
           int cx = 0, cy = 0, cz = 0;
           const int j = my_c ? __ffs(my_c) - 1 : 0;
@@ -812,11 +836,14 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
             const int sx = __shfl_sync(0xffffffffu, cx, src);
             const int sy = __shfl_sync(0xffffffffu, cy, src);
             const int sz = __shfl_sync(0xffffffffu, cz, src);
-            const int sum =
-                __reduce_add_sync(0xffffffffu, lc_tap_share<CHECKED>(V, F, sx, sy, sz, lane));
+            const int sum = __reduce_add_sync(
+                0xffffffffu, KIND == VX_FILTER_MEAN ? mean_tap_share<CHECKED>(V, F, sx, sy, sz, lane)
+                                                    : lc_tap_share<CHECKED>(V, F, sx, sy, sz, lane));
             if ((int)lane == src) {
               VX_DIAG(dFilter);
-              if (__ddiv_rn((double)sum, (double)(27 * F.M)) >= M.T) {
+              const double den = KIND == VX_FILTER_MEAN ? (double)(F.M * F.M * F.M)
+                                                        : (double)(27 * F.M);
+              if (__ddiv_rn((double)sum, den) >= M.T) {
                 VX_DIAG(dHit);
                 ht = sample_t(base, M.s, k + j);
                 k += j;

@@ -21,7 +21,6 @@ base = min(samples)
 line_of = {}
 cur = None
 inside = False
-src_file = None
 for l in open(dump):
     if l.startswith("//----") and ".text." in l:
         inside = kname in l
@@ -30,8 +29,7 @@ for l in open(dump):
         continue
     m = re.search(r'//## File "([^"]+)", line (\d+)', l)
     if m:
-        cur = int(m.group(2))
-        src_file = m.group(1)
+        cur = (m.group(1), int(m.group(2)))
         continue
     m = re.match(r"\s+/\*([0-9a-f]{4,})\*/", l)
     if m and cur is not None:
@@ -43,7 +41,23 @@ for a, (s, i) in samples.items():
     agg[ln][1] += i
 ts = sum(v[0] for v in agg.values()) or 1
 ti = sum(v[1] for v in agg.values()) or 1
-src = open(sys.argv[5] if len(sys.argv) > 5 else src_file).read().splitlines() if src_file else []
-for ln, (s, i) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
-    text = src[ln - 1].strip()[:90] if ln and ln <= len(src) else "?"
-    print(f"{ln!s:>5} stall {100*s/ts:5.1f}% inst {100*i/ti:5.1f}%  {text}")
+srcs = {}
+
+
+def text_of(key):
+    if not key:
+        return "?", "?"
+    f, ln = key
+    if f not in srcs:
+        try:
+            srcs[f] = open(f).read().splitlines()
+        except OSError:
+            srcs[f] = []
+    src = srcs[f]
+    name = f"{f.rsplit('/', 1)[-1]}:{ln}"
+    return name, (src[ln - 1].strip()[:80] if ln <= len(src) else "?")
+
+
+for key, (s, i) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+    name, text = text_of(key)
+    print(f"{name:>28} stall {100*s/ts:5.1f}% inst {100*i/ti:5.1f}%  {text}")
