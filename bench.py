@@ -47,7 +47,7 @@ METRIC = "filtered frames/s (ms/frame) at 1024² on 1024³ CT; Otsu hist GB/s vs
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--size", type=int, default=1024, help="volume edge (voxels)")
