@@ -73,6 +73,14 @@ constexpr bool kSplitRays = VX_SPLIT_RAYS && kWarpsPerBlock == 4;
 // C2, 32: +3 %)
 #define VX_COOP_MEAN 4
 #endif
+#ifndef VX_COOP_SIGMA
+// the same for sigma: 4 -> C1 -11 %, C2/C3 -3.8 % (2: -11 % / -2.9 %)
+#define VX_COOP_SIGMA 4
+#endif
+#ifndef VX_COOP_ENTROPY
+// entropy (M = 3 only: one term per lane): 4 -> C1 -11 %, C3 -4.5 %
+#define VX_COOP_ENTROPY 4
+#endif
 #ifndef VX_GROUP_PIPE
 #define VX_GROUP_PIPE 0
 #endif
@@ -369,6 +377,29 @@ __device__ __forceinline__ int mean_tap_share(const VolView& V, const FiltD& F, 
     const int dy = (M == 3) ? r / 3 : r / M;
     const int dx = r - dy * M;
     s += rd<CHECKED>(V, x + dx - h, y + dy - h, z + dz - h);
+  }
+  return s;
+}
+
+// This lane's share of filter_sigma's (sum, count) over the M^3 box: voxels
+// within the band of the centre value c.
+template <bool CHECKED>
+__device__ __forceinline__ int sigma_tap_share(const VolView& V, const FiltD& F, int x, int y,
+                                               int z, int c, unsigned lane, int& cnt) {
+  const int M = F.M, h = (M - 1) >> 1;
+  int s = 0;
+  cnt = 0;
+  for (int t = (int)lane; t < M * M * M; t += 32) {
+    const int dz = (M == 3) ? t / 9 : t / (M * M);
+    const int r = t - dz * M * M;
+    const int dy = (M == 3) ? r / 3 : r / M;
+    const int dx = r - dy * M;
+    const int v = rd<CHECKED>(V, x + dx - h, y + dy - h, z + dz - h);
+    const int diff = v > c ? v - c : c - v;
+    if ((double)diff <= F.band) {
+      s += v;
+      ++cnt;
+    }
   }
   return s;
 }
@@ -808,10 +839,12 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
       unsigned rem = 0;
       bool coop = false;
       constexpr int kCoop = KIND == VX_FILTER_LOCAL_CLUSTER ? VX_COOP_FIRST
-                            : (KIND == VX_FILTER_MEAN ? VX_COOP_MEAN : 0);
+                            : KIND == VX_FILTER_MEAN ? VX_COOP_MEAN
+                            : KIND == VX_FILTER_SIGMA ? VX_COOP_SIGMA
+                            : KIND == VX_FILTER_ENTROPY ? VX_COOP_ENTROPY : 0;
       if (kCoop) {
         const unsigned fm = __ballot_sync(0xffffffffu, need && my_c);
-        coop = fm != 0 && __popc(fm) <= kCoop;
+        coop = fm != 0 && __popc(fm) <= kCoop && (KIND != VX_FILTER_ENTROPY || F.M == 3);
         if (coop) {
           int cx = 0, cy = 0, cz = 0;
           const int j = my_c ? __ffs(my_c) - 1 : 0;
@@ -836,14 +869,43 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
             const int sx = __shfl_sync(0xffffffffu, cx, src);
             const int sy = __shfl_sync(0xffffffffu, cy, src);
             const int sz = __shfl_sync(0xffffffffu, cz, src);
-            const int sum = __reduce_add_sync(
-                0xffffffffu, KIND == VX_FILTER_MEAN ? mean_tap_share<CHECKED>(V, F, sx, sy, sz, lane)
-                                                    : lc_tap_share<CHECKED>(V, F, sx, sy, sz, lane));
+            double f;
+            if (KIND == VX_FILTER_ENTROPY) {
+              // lane i loads term i of the 27 (kernel_offsets order: dx outer,
+              // dy, dz inner); the ordered FP64 sum is then formed by every
+              // lane from broadcasts, in filter_entropy's sequence
+              double term = 0.0;
+              if (lane < 27) {
+                const int dx = (int)lane / 9 - 1, dy = ((int)lane / 3) % 3 - 1,
+                          dz = (int)lane % 3 - 1;
+                term = lut[rd<CHECKED>(V, sx + dx, sy + dy, sz + dz)];
+              }
+              double H = __shfl_sync(0xffffffffu, term, 0);
+#pragma unroll
+              for (int i = 1; i < 27; ++i) H = __dadd_rn(H, __shfl_sync(0xffffffffu, term, i));
+              f = H > F.entropy_t ? (double)rd<CHECKED>(V, sx, sy, sz) : 0.0;
+            } else {
+              int part, pcnt = 0;
+              if (KIND == VX_FILTER_MEAN) {
+                part = mean_tap_share<CHECKED>(V, F, sx, sy, sz, lane);
+              } else if (KIND == VX_FILTER_SIGMA) {
+                // every lane reads the centre itself (one L1-resident byte)
+                part = sigma_tap_share<CHECKED>(V, F, sx, sy, sz, rd<CHECKED>(V, sx, sy, sz),
+                                                lane, pcnt);
+              } else {
+                part = lc_tap_share<CHECKED>(V, F, sx, sy, sz, lane);
+              }
+              const int sum = __reduce_add_sync(0xffffffffu, part);
+              const int cnt =
+                  KIND == VX_FILTER_SIGMA ? __reduce_add_sync(0xffffffffu, pcnt) : 0;
+              const double den = KIND == VX_FILTER_MEAN    ? (double)(F.M * F.M * F.M)
+                                 : KIND == VX_FILTER_SIGMA ? (double)cnt  // centre qualifies
+                                                           : (double)(27 * F.M);
+              f = __ddiv_rn((double)sum, den);
+            }
             if ((int)lane == src) {
               VX_DIAG(dFilter);
-              const double den = KIND == VX_FILTER_MEAN ? (double)(F.M * F.M * F.M)
-                                                        : (double)(27 * F.M);
-              if (__ddiv_rn((double)sum, den) >= M.T) {
+              if (f >= M.T) {
                 VX_DIAG(dHit);
                 ht = sample_t(base, M.s, k + j);
                 k += j;

@@ -228,7 +228,7 @@ def test_random_cameras_steps_thresholds_vs_oracle(vx, oracle):
 
 def test_cluster_and_mean_kernel_sizes_vs_oracle(vx, oracle):
     """Local cluster at M = 3/5/7 and d = 1-4 (filters.py:154-184), box mean
-    at M = 3/5/7 (filters.py:173-174): the march's first-candidate evaluation
+    and sigma at M = 3/5/7 (filters.py:173-195): the march's first-candidate evaluation
     splits the taps over the warp when few lanes need it, and must give the
     oracle's hit voxels and pixels."""
     from paper_1807_03119_b200.render import render_detail
@@ -245,11 +245,12 @@ def test_cluster_and_mean_kernel_sizes_vs_oracle(vx, oracle):
         w, hh = 48, 40
         params = vx.RenderParams(width=w, height=hh, step_size=0.5)
         cv = oracle.cam_vector(pos, (22.0, 20.0, 18.0), w, hh, fov_y_deg=40.0)
-        for kind, T in (("local-cluster", 100.0), ("local-cluster", 150.0), ("mean", 120.0)):
+        for kind, T in (("local-cluster", 100.0), ("local-cluster", 150.0), ("mean", 120.0),
+                        ("sigma", 120.0)):
             cfg = vx.FilterConfig(kind=vx.FilterKind.from_name(kind), threshold=T, kernel_size=m,
                                   cluster_offset=d)
-            want = oracle.render(data, cv, w, hh, kind=kind, threshold=T,
-                                 kernel_size=m, cluster_offset=d)
+            want = oracle.render(data, cv, w, hh, kind=kind, threshold=T, kernel_size=m,
+                                 cluster_offset=d, sigma_band=2.0 * h.global_sigma)
             for skip in (True, True, False):
                 got = render_detail(v, cam, params, cfg, h, diagnostics=True, skip=skip)
                 assert np.array_equal(got.hit_voxel, want["hit_voxel"]), (trial, kind, m, d, T, skip)
