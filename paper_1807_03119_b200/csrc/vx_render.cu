@@ -1584,8 +1584,12 @@ int make_march(const vx_volume* v, const vx_render_params* rp, const vx_filter_c
   M.step = rp->step_size;
   M.skip = rp->skip && thr > 0 && thr <= 255;
   {
+    // D = 1 (the empty cell itself, at most 4 voxels of the ray): one
+    // sample group (8 samples) covers it when step >= 0.5, cheaper than a
+    // lookup + skip + re-lookup.  Measured at step 0.5: 2 vs 1 -> bench
+    // frame -4 %, C2 LC -7 %, C1 -8..-13 %, C4 -4 %; 3 is slower everywhere
     const char* e = getenv("VOXB200_SKIP_MIN_D");
-    M.skip_min_d = e ? atoi(e) : 1;
+    M.skip_min_d = e ? atoi(e) : (rp->step_size >= 0.5 ? 2 : 1);
     if (M.skip_min_d < 1) M.skip_min_d = 1;
   }
   return VX_OK;
