@@ -793,10 +793,13 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
         }
       };
       // passes issued back to back: 4 where rejected candidates are common
-      // (sigma, entropy), 2 elsewhere (measured: local cluster -3 % on the
-      // bench frame with 2, entropy +2.6 %); VX_GROUP_PIPE forces one depth
+      // (sigma, entropy), 2 for local cluster (measured: -3 % on the bench
+      // frame with 2, entropy +2.6 %); VX_GROUP_PIPE forces one depth
+      // Re-measured with distance-1 cells sampled (skip_min_d 2): 4 for
+      // none/mean/okada too (C1 -5 %, C2 mean -3 %, okada -1.5 %), local
+      // cluster stays at 2 (4: bench +1.7 %, C2 +3.8 %, C4 +1.3 %)
       constexpr int kPipe = VX_GROUP_PIPE ? VX_GROUP_PIPE
-                            : (KIND == VX_FILTER_ENTROPY || KIND == VX_FILTER_SIGMA ? 4 : 2);
+                            : (KIND == VX_FILTER_LOCAL_CLUSTER ? 2 : 4);
       if (kPipe == 4) {
       for (int b = 0; b < nr; b += 16) {
         int raw0, raw1 = 0, raw2 = 0, raw3 = 0;
