@@ -168,7 +168,12 @@ int vx_histogram_host(const uint8_t* host, uint64_t n, uint64_t counts_out[256])
  * asynchronously on `stream` (a cudaStream_t used as given: 0 is the legacy default
  * stream, so work queued by torch on its default stream is ordered before it). */
 int vx_histogram_device(const uint8_t* dev, uint64_t n, uint64_t* dev_counts, void* stream);
-/* K2: exact Otsu threshold (256-bit cross-multiplied argmin, ties -> smallest
+/* K1 over the z-planes [z0, z1) of a replica, accumulated into dev_counts[256]
+ * asynchronously on `stream`: the z-slab shard of the multi-GPU histogram
+ * (SURVEY.md §8e); every rank counts its slab of the replica it holds. */
+int vx_volume_histogram_slab(vx_volume* vol, int64_t z0, int64_t z1, uint64_t* dev_counts,
+                             void* stream);
+/* K2: exact Otsu threshold (320-bit cross-multiplied argmin, ties -> smallest
  * T) of histogram.py:59-101; total must be < 2^47. */
 int vx_otsu(const uint64_t counts[256], int32_t* T_out);
 /* K2 on device counts; writes the threshold to dev_T (int32) */
@@ -217,6 +222,58 @@ int vx_sobel_batch(vx_volume* vol, const int64_t* xs, const int64_t* ys, const i
 /* shade_phong_batch (render.py:385-403) */
 int vx_phong_batch(const double* normals, const double* view_dirs, int64_t n,
                    const vx_render_params* rp, uint8_t* out);
+
+/* ---- multi-GPU frame group -------------------------------
+ * The multi-GPU comm init of SURVEY.md §8b's `vx_init`: sort-first rendering
+ * over `world` ranks (one process or one thread per GPU, same node), the
+ * reference's worker-band split (render.py:514-541, bit-identical for any
+ * worker count, test_render.py:242-251) at GPU granularity.  Every rank holds
+ * a full replica (vx_volume_*), renders the 8x16 tiles t with t % world ==
+ * rank, and its K4 stores them straight into rank 0's frame slot over
+ * NVLink (peer / CUDA-IPC pointers); the image histogram, hit count and
+ * samples are added there with system-scope atomics.  No collective per
+ * frame: completion and slot reuse are monotonic flags written and awaited
+ * with stream memory operations (VX_GROUP_SYNC_DEVICE), or ordered by the
+ * caller's host barrier (VX_GROUP_SYNC_HOST: ranks sharing one GPU).
+ *
+ *   vx_group_create    -> this rank's blob (VX_GROUP_BLOB_BYTES)
+ *   (caller all-gathers the blobs in rank order: MPI, torch.distributed, ...)
+ *   vx_group_connect   opens the peers' blocks (IPC, or peer access in-process)
+ *   per frame, every rank: vx_group_render; rank 0 then consumes the frame
+ *   (vx_group_download or its device pointers) and calls vx_group_release.
+ */
+#define VX_GROUP_BLOB_BYTES 256
+enum vx_group_sync {
+  VX_GROUP_SYNC_AUTO = -1,  /* device flags when every rank has its own GPU   */
+  VX_GROUP_SYNC_DEVICE = 0, /* stream-memop flags, no host round trip         */
+  VX_GROUP_SYNC_HOST = 1    /* caller orders frames (stream sync + barrier)   */
+};
+typedef struct vx_group vx_group;
+typedef struct {
+  uint8_t* pixels;    /* device pointer (rank 0's slot), height*width       */
+  uint64_t* counters; /* device: [256] image histogram, [256] hits,
+                         [257] samples, [258] truncation flag (int32)        */
+  uint32_t frame;     /* 1-based frame number of this rank                   */
+  uint32_t _pad;
+} vx_group_frame;
+int vx_group_create(int32_t rank, int32_t world, int64_t max_pixels, vx_group** out,
+                    uint8_t* blob_out);
+int vx_group_connect(vx_group* g, const uint8_t* blobs, int32_t sync);
+int vx_group_info(const vx_group* g, int32_t* sync_out, uint32_t* frame_out);
+/* This rank's tiles of the next frame, asynchronously on `stream`.  On rank 0
+ * (device sync) the stream then waits for every rank's tiles: work queued
+ * behind this call sees the whole frame.  Rank 0 may hold at most two
+ * unreleased frames. */
+int vx_group_render(vx_group* g, vx_volume* vol, const vx_ray_setup* rs,
+                    const vx_render_params* rp, const vx_filter_config* fc, void* stream,
+                    vx_group_frame* out);
+/* rank 0: the oldest unreleased frame is consumed: zero its counters and
+ * hand its slot back to the peers (stream-ordered).  No-op on other ranks. */
+int vx_group_release(vx_group* g, void* stream);
+/* rank 0: copy the oldest unreleased frame to host memory and synchronise */
+int vx_group_download(vx_group* g, uint8_t* host_pixels, uint64_t* host_counters,
+                      int64_t n_pixels, void* stream);
+int vx_group_destroy(vx_group* g);
 
 /* ---- phantom input generator (volume.py:317-368; inputs only) ------------ */
 /* shape kinds: 0 sphere, 1 shell, 2 box; params per shape:

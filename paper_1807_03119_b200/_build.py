@@ -15,7 +15,7 @@ CSRC = PKG / "csrc"
 LIB = PKG / "libvoxb200.so"
 INCLUDE = PKG.parent / "include"
 
-SOURCES = ["vx_api.cu", "vx_hist.cu", "vx_volume.cu", "vx_render.cu", "vx_io.cu"]
+SOURCES = ["vx_api.cu", "vx_hist.cu", "vx_volume.cu", "vx_render.cu", "vx_io.cu", "vx_group.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -102,6 +102,18 @@ class vx_render_out(C.Structure):
     ]
 
 
+class vx_group_frame(C.Structure):
+    _fields_ = [
+        ("pixels", C.c_void_p),
+        ("counters", C.c_void_p),
+        ("frame", C.c_uint32),
+        ("_pad", C.c_uint32),
+    ]
+
+
+VX_GROUP_BLOB_BYTES = 256
+VX_GROUP_SYNC_AUTO, VX_GROUP_SYNC_DEVICE, VX_GROUP_SYNC_HOST = -1, 0, 1
+
 P = C.c_void_p
 I32, I64, U64, F64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double
 
@@ -146,6 +158,14 @@ SIGNATURES = {
     "vx_host_alloc": [U64, P],
     "vx_host_free": [P],
     "vx_volume_distance_map": [P, I32, I32, P, P],
+    "vx_volume_histogram_slab": [P, I64, I64, P, P],
+    "vx_group_create": [I32, I32, I64, P, P],
+    "vx_group_connect": [P, P, I32],
+    "vx_group_info": [P, P, P],
+    "vx_group_render": [P, P, P, P, P, P, P],
+    "vx_group_release": [P, P],
+    "vx_group_download": [P, P, P, I64, P],
+    "vx_group_destroy": [P],
 }
 _RESTYPES = {"vx_last_error": C.c_char_p}
 

@@ -16,8 +16,9 @@
 // errors / context
 
 static thread_local char tl_error[512] = "";
-static thread_local cudaStream_t tl_stream = nullptr;
-static thread_local int tl_stream_device = -1;
+// one stream per (thread, device), kept for the thread's life: switching
+// devices and back keeps work on a device ordered on one stream
+static thread_local cudaStream_t tl_stream[64] = {};
 static thread_local uint64_t tl_launches = 0;
 
 void vx_set_error(const char* fmt, ...) {
@@ -38,9 +39,9 @@ void vx_count_launch() { ++tl_launches; }
 cudaStream_t vx_stream() {
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!tl_stream || tl_stream_device != dev) {
-    cudaStreamCreateWithFlags(&tl_stream, cudaStreamNonBlocking);
-    tl_stream_device = dev;
+  cudaStream_t& st = tl_stream[dev & 63];
+  if (!st) {
+    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
     // keep freed stream-ordered scratch cached in the pool
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
@@ -48,7 +49,7 @@ cudaStream_t vx_stream() {
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
   }
-  return tl_stream;
+  return st;
 }
 
 int vx_sm_count() {
@@ -166,13 +167,14 @@ int vx_volume_alloc(int64_t nx, int64_t ny, int64_t nz, vx_volume** out) {
   v->csy = v->ncx + 2;
   v->csz = (int64_t)(v->ncx + 2) * (v->ncy + 2);
   v->cmap_bytes = (uint64_t)v->csz * (v->ncz + 2);
-  for (auto& d : v->dist) {
-    d.thr = -1;
-    d.map = nullptr;  // slots assigned below
-    d.stamp = 0;
-  }
-  cudaError_t e = cudaMalloc(&v->alloc, v->alloc_bytes);
+  cudaError_t e = cudaEventCreateWithFlags(&v->scratch_done, cudaEventDisableTiming);
   if (e != cudaSuccess) {
+    delete v;
+    return vx_cuda_fail(e, "cudaEventCreate", __FILE__, __LINE__);
+  }
+  e = cudaMalloc(&v->alloc, v->alloc_bytes);
+  if (e != cudaSuccess) {
+    cudaEventDestroy(v->scratch_done);
     delete v;
     return vx_cuda_fail(e, "cudaMalloc(volume)", __FILE__, __LINE__);
   }
@@ -180,6 +182,7 @@ int vx_volume_alloc(int64_t nx, int64_t ny, int64_t nz, vx_volume** out) {
   e = cudaMalloc(&v->bmax, slot * (1 + VX_DIST_CACHE + VX_ACC_CACHE) + 2 * v->cmap_bytes);
   if (e != cudaSuccess) {
     cudaFree(v->alloc);
+    cudaEventDestroy(v->scratch_done);
     delete v;
     return vx_cuda_fail(e, "cudaMalloc(brick map)", __FILE__, __LINE__);
   }
@@ -231,7 +234,11 @@ int vx_volume_finish(vx_volume* v, const uint8_t* compact_dev, cudaStream_t s) {
     int32_t T;
     memcpy(&T, &th[256], 4);
     const uint8_t* m = nullptr;
-    if (T > 0 && T <= 255 && (rc = vx_get_dist_map(v, T, &m, s))) return rc;
+    MapSlot* slot = nullptr;
+    if (T > 0 && T <= 255) {
+      if ((rc = vx_get_dist_map(v, T, &m, &slot, s))) return rc;
+      if ((rc = vx_map_release(v, slot, s))) return rc;
+    }
     if ((rc = vx_preload_render_kernels())) return rc;
     // grow the stream-ordered pool once (it keeps freed memory: release
     // threshold above), so a first frame's staging comes from retained memory
@@ -369,6 +376,13 @@ extern "C" int vx_volume_destroy(vx_volume* v) {
   cudaGetDevice(&cur);
   if (cur != v->device) cudaSetDevice(v->device);
   cudaDeviceSynchronize();
+  auto drop = [](MapSlot& m) {
+    if (m.ready) cudaEventDestroy(m.ready);
+    for (auto& u : m.uses) cudaEventDestroy(u.ev);
+  };
+  for (auto& d : v->dist) drop(d);
+  for (auto& a : v->acc) drop(a);
+  if (v->scratch_done) cudaEventDestroy(v->scratch_done);
   if (v->bmax) cudaFree(v->bmax);
   if (v->alloc) cudaFree(v->alloc);
   if (cur != v->device) cudaSetDevice(cur);
@@ -414,34 +428,80 @@ extern "C" int vx_volume_read(const vx_volume* v, uint8_t* host_out) {
   return VX_OK;
 }
 
-int vx_get_dist_map(vx_volume* v, int thr, const uint8_t** map_out, cudaStream_t s) {
+int vx_map_claim(vx_volume* v, MapSlot* m, cudaStream_t s) {
+  for (auto& u : m->uses) VX_CUDA(cudaStreamWaitEvent(s, u.ev, 0));
+  VX_CUDA(cudaStreamWaitEvent(s, v->scratch_done, 0));
+  return VX_OK;
+}
+
+int vx_map_publish(vx_volume* v, MapSlot* m, cudaStream_t s) {
+  if (!m->ready) VX_CUDA(cudaEventCreateWithFlags(&m->ready, cudaEventDisableTiming));
+  VX_CUDA(cudaEventRecord(m->ready, s));
+  VX_CUDA(cudaEventRecord(v->scratch_done, s));
+  return VX_OK;
+}
+
+int vx_map_pin(MapSlot* m, cudaStream_t s) {
+  if (m->ready) VX_CUDA(cudaStreamWaitEvent(s, m->ready, 0));
+  ++m->pins;
+  return VX_OK;
+}
+
+int vx_map_release(vx_volume* v, MapSlot* m, cudaStream_t s) {
+  if (!m) return VX_OK;
+  std::lock_guard<std::mutex> lock(v->mu);
+  --m->pins;
+  MapUse* use = nullptr;
+  for (auto& u : m->uses)
+    if (u.stream == s) use = &u;
+  if (!use) {
+    MapUse u;
+    u.stream = s;
+    VX_CUDA(cudaEventCreateWithFlags(&u.ev, cudaEventDisableTiming));
+    m->uses.push_back(u);
+    use = &m->uses.back();
+  }
+  VX_CUDA(cudaEventRecord(use->ev, s));
+  return VX_OK;
+}
+
+int vx_get_dist_map(vx_volume* v, int thr, const uint8_t** map_out, MapSlot** slot_out,
+                    cudaStream_t s) {
+  *map_out = nullptr;
+  *slot_out = nullptr;
   std::lock_guard<std::mutex> lock(v->mu);
   ++v->stamp;
   for (auto& d : v->dist) {
     if (d.thr >= 0 && d.thr == thr) {
       d.stamp = v->stamp;
+      int rc = vx_map_pin(&d, s);
+      if (rc) return rc;
       *map_out = d.map;
+      *slot_out = &d;
       return VX_OK;
     }
   }
-  DistEntry* victim = &v->dist[0];
+  DistEntry* victim = nullptr;
   for (auto& d : v->dist) {
+    if (d.pins) continue;  // a render between lookup and launch still needs it
     if (d.thr < 0) {
       victim = &d;
       break;
     }
-    if (d.stamp < victim->stamp) victim = &d;
+    if (!victim || d.stamp < victim->stamp) victim = &d;
   }
-  // another thread's stream may still read the evicted map
-  if (victim->thr >= 0) VX_CUDA(cudaDeviceSynchronize());
+  if (!victim) return VX_OK;  // every slot in flight: this frame renders without skipping
   victim->thr = -1;
-  int rc = vx_launch_dist_map(v, thr, victim->map, s);
+  int rc = vx_map_claim(v, victim, s);  // after every K4 that read the old map
   if (rc) return rc;
-  // other streams may pick this map up: make it visible before publishing
-  VX_CUDA(cudaStreamSynchronize(s));
+  rc = vx_launch_dist_map(v, thr, victim->map, s);
+  if (rc) return rc;
+  if ((rc = vx_map_publish(v, victim, s))) return rc;
+  if ((rc = vx_map_pin(victim, s))) return rc;
   victim->thr = thr;
   victim->stamp = v->stamp;
   *map_out = victim->map;
+  *slot_out = victim;
   return VX_OK;
 }
 
@@ -459,10 +519,18 @@ extern "C" int vx_volume_distance_map(vx_volume* v, int32_t thr, int32_t level,
   if (!host_out) return VX_OK;
   cudaStream_t s = vx_stream();
   const uint8_t* map = nullptr;
-  int rc = vx_get_dist_map(v, thr, &map, s);
+  MapSlot* slot = nullptr;
+  int rc = vx_get_dist_map(v, thr, &map, &slot, s);
   if (rc) return rc;
-  VX_CUDA(cudaMemcpyAsync(host_out, level ? map + v->map_bytes : map,
-                          level ? v->cmap_bytes : v->map_bytes, cudaMemcpyDeviceToHost, s));
+  if (!map) {
+    vx_set_error("vx_volume_distance_map: every map slot is in use");
+    return VX_EINVAL;
+  }
+  cudaError_t e = cudaMemcpyAsync(host_out, level ? map + v->map_bytes : map,
+                                  level ? v->cmap_bytes : v->map_bytes, cudaMemcpyDeviceToHost, s);
+  rc = vx_map_release(v, slot, s);
+  if (e != cudaSuccess) return vx_cuda_fail(e, "cudaMemcpyAsync(map)", __FILE__, __LINE__);
+  if (rc) return rc;
   VX_CUDA(cudaStreamSynchronize(s));
   return VX_OK;
 }
@@ -487,6 +555,23 @@ extern "C" int vx_histogram_device(const uint8_t* dev, uint64_t n, uint64_t* dev
   }
   cudaStream_t s = (cudaStream_t)stream;
   return vx_launch_hist(dev, n, dev_counts, s);
+}
+
+extern "C" int vx_volume_histogram_slab(vx_volume* v, int64_t z0, int64_t z1, uint64_t* dev_counts,
+                                        void* stream) {
+  if (!v || !dev_counts || z0 < 0 || z1 > v->nz || z0 > z1) {
+    vx_set_error("vx_volume_histogram_slab: bad argument (planes [%lld, %lld) of %d)",
+                 (long long)z0, (long long)z1, v ? v->nz : 0);
+    return VX_EINVAL;
+  }
+  if (z0 == z1) return VX_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  // whole padded planes are contiguous: count them, then take the apron's
+  // zeros (every padded plane holds sz - nx*ny of them) out of bin 0
+  const uint64_t planes = (uint64_t)(z1 - z0);
+  int rc = vx_launch_hist(v->alloc + (uint64_t)(z0 + VX_PAD) * v->sz, planes * v->sz, dev_counts, s);
+  if (rc) return rc;
+  return vx_launch_sub_bin0(dev_counts, planes * ((uint64_t)v->sz - (uint64_t)v->nx * v->ny), s);
 }
 
 extern "C" int vx_histogram_host(const uint8_t* host, uint64_t n, uint64_t counts_out[256]) {
@@ -544,7 +629,7 @@ extern "C" int vx_otsu(const uint64_t counts[256], int32_t* T_out) {
     return VX_EINVAL;
   }
   if (total >= ((unsigned __int128)1 << 47)) {
-    vx_set_error("histogram total %.3e exceeds the exact 256-bit Otsu range (2^47)",
+    vx_set_error("histogram total %.3e exceeds the exact 320-bit Otsu range (2^47)",
                  (double)total);
     return VX_ERANGE;
   }

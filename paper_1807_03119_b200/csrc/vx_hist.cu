@@ -446,21 +446,39 @@ __device__ double pairwise(const double* a, int n) {
   return __dadd_rn(pw_level(a, n2), pw_level(a + n2, n - n2));
 }
 
-__global__ void entropy_kernel(const unsigned long long* __restrict__ counts, uint64_t n,
-                               double* __restrict__ H_out) {
+// 256 threads: bin b's term p*log2(p) on thread b (the FP64 log2 is the
+// cost: one thread doing all 256 took ~60 us), compacted in bin order over
+// the non-empty bins, then thread 0 adds them in numpy's pairwise order
+// (~256 dependent FP64 adds).
+__global__ void __launch_bounds__(256) entropy_kernel(const unsigned long long* __restrict__ counts,
+                                                      uint64_t n, double* __restrict__ H_out) {
   __shared__ double terms[256];
-  if (threadIdx.x != 0) return;
-  int k = 0;
-  const double dn = (double)n;
-  for (int b = 0; b < 256; ++b) {
-    unsigned long long c = counts[b];
-    if (c) {
-      double p = __ddiv_rn((double)c, dn);
-      terms[k++] = __dmul_rn(p, log2(p));
-    }
+  __shared__ int warp_base[9];
+  const int b = threadIdx.x;
+  const unsigned long long c = counts[b];
+  double t = 0.0;
+  if (c) {
+    const double p = __ddiv_rn((double)c, (double)n);
+    t = __dmul_rn(p, log2(p));
   }
-  double s = pairwise(terms, k);
-  *H_out = -s;
+  const unsigned m = __ballot_sync(0xffffffffu, c != 0);
+  const int w = b >> 5, lane = b & 31;
+  if (lane == 0) warp_base[w + 1] = __popc(m);
+  __syncthreads();
+  if (b == 0) {
+    warp_base[0] = 0;
+    for (int i = 1; i <= 8; ++i) warp_base[i] += warp_base[i - 1];
+  }
+  __syncthreads();
+  if (c) terms[warp_base[w] + __popc(m & ((1u << lane) - 1u))] = t;
+  __syncthreads();
+  if (b == 0) *H_out = -pairwise(terms, warp_base[8]);
+}
+
+// bin 0 of a slab histogram counted over whole padded planes: minus the
+// apron's zeros (vx_volume_histogram_slab)
+__global__ void sub_bin0_kernel(unsigned long long* counts, unsigned long long v) {
+  counts[0] -= v;
 }
 
 }  // namespace
@@ -531,7 +549,14 @@ int vx_launch_otsu(const uint64_t* dev_counts, int32_t* dev_T, cudaStream_t s) {
 }
 
 int vx_launch_entropy(const uint64_t* dev_counts, uint64_t n, double* dev_H, cudaStream_t s) {
-  entropy_kernel<<<1, 32, 0, s>>>(reinterpret_cast<const unsigned long long*>(dev_counts), n, dev_H);
+  entropy_kernel<<<1, 256, 0, s>>>(reinterpret_cast<const unsigned long long*>(dev_counts), n, dev_H);
+  VX_CHECK_LAUNCH();
+  return VX_OK;
+}
+
+int vx_launch_sub_bin0(uint64_t* dev_counts, uint64_t v, cudaStream_t s) {
+  if (!v) return VX_OK;
+  sub_bin0_kernel<<<1, 1, 0, s>>>(reinterpret_cast<unsigned long long*>(dev_counts), v);
   VX_CHECK_LAUNCH();
   return VX_OK;
 }

@@ -6,6 +6,7 @@
 
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/voxb200.h"
 
@@ -58,10 +59,27 @@ struct VolView {
   int64_t csy, csz;       // strides of the cell maps
 };
 
-struct DistEntry {
-  int thr;       // -1: empty
-  uint8_t* map;  // slot in vx_volume::bmax: brick map (map_bytes) then cell map (cmap_bytes)
-  uint64_t stamp;
+// Lifetime of a cached map slot (distance or accepted-cell map).  A render
+// pins the slot from its lookup until its K4 is enqueued, then records the
+// slot's per-stream use event behind that K4 and unpins it.  Eviction takes
+// only unpinned slots and orders the rebuild (on the evicting thread's
+// stream) after every recorded use; a freshly built map is published with a
+// `ready` event that other streams wait on.  No host synchronisation happens
+// under the volume mutex.
+struct MapUse {
+  cudaStream_t stream;
+  cudaEvent_t ev;
+};
+struct MapSlot {
+  uint8_t* map = nullptr;  // slot in vx_volume::bmax: brick map (map_bytes) then cell map (cmap_bytes)
+  uint64_t stamp = 0;
+  int pins = 0;
+  cudaEvent_t ready = nullptr;
+  std::vector<MapUse> uses;
+};
+
+struct DistEntry : MapSlot {
+  int thr = -1;  // -1: empty
 };
 
 // Accepted-cell distance maps: the skip structure of one filter setting.
@@ -69,12 +87,10 @@ struct DistEntry {
 // compared exactly).  valid && !built: the key was seen once (not built yet).
 #define VX_ACC_CACHE 4
 #define VX_ACC_KEY_BYTES 2096
-struct AccEntry {
+struct AccEntry : MapSlot {
   bool valid = false;
   bool built = false;
   unsigned char key[VX_ACC_KEY_BYTES];
-  uint8_t* map = nullptr;  // slot in vx_volume::bmax: brick map (zeros) then cell map
-  uint64_t stamp = 0;
 };
 
 struct vx_volume {
@@ -101,16 +117,30 @@ struct vx_volume {
   DistEntry dist[VX_DIST_CACHE];
   AccEntry acc[VX_ACC_CACHE];
   // two cell-map-sized scratch regions for the map builds (occupancy and the
-  // distance passes' intermediate), used under `mu`
+  // distance passes' intermediate), claimed under `mu`; builds on different
+  // streams are ordered through scratch_done
   uint8_t* scratch;
+  cudaEvent_t scratch_done;
   uint64_t stamp;
   uint64_t counts[256];
   std::mutex mu;
 };
 
 VolView vx_view(const vx_volume* v, const uint8_t* dist_map);
-// returns the (cached) distance map of thr, building it if needed
-int vx_get_dist_map(vx_volume* v, int thr, const uint8_t** map_out, cudaStream_t s);
+// The (cached) distance map of thr, built if needed (stream-ordered on s),
+// pinned: pass *slot_out to vx_map_release once the work reading it is
+// enqueued on s.  *map_out == nullptr (no skipping) when every slot is pinned.
+int vx_get_dist_map(vx_volume* v, int thr, const uint8_t** map_out, MapSlot** slot_out,
+                    cudaStream_t s);
+// caller holds v->mu: the slot is being reused for a new map; order stream s
+// after every recorded reader and after earlier builds' use of the scratch
+int vx_map_claim(vx_volume* v, MapSlot* m, cudaStream_t s);
+// caller holds v->mu: the slot's map (built on s) is complete on s
+int vx_map_publish(vx_volume* v, MapSlot* m, cudaStream_t s);
+// caller holds v->mu: stream s will read the slot's map (waits for its build)
+int vx_map_pin(MapSlot* m, cudaStream_t s);
+// unpin after the readers on s are enqueued (nullptr: no-op)
+int vx_map_release(vx_volume* v, MapSlot* m, cudaStream_t s);
 
 // launchers implemented across translation units
 int vx_launch_hist(const uint8_t* dev, uint64_t n, uint64_t* dev_counts, cudaStream_t s);
@@ -118,6 +148,7 @@ int vx_launch_otsu(const uint64_t* dev_counts, int32_t* dev_T, cudaStream_t s);
 // K1+K2 fused: dev_counts[256] overwritten, dev_T = Otsu T (-1: empty / >= 2^47)
 int vx_launch_hist_otsu(const uint8_t* dev, uint64_t n, uint64_t* dev_counts, int32_t* dev_T,
                         cudaStream_t s);
+int vx_launch_sub_bin0(uint64_t* dev_counts, uint64_t v, cudaStream_t s);
 int vx_launch_entropy(const uint64_t* dev_counts, uint64_t n, double* dev_H, cudaStream_t s);
 int vx_launch_brick_max(vx_volume* v, cudaStream_t s);
 int vx_launch_dist_map(const vx_volume* v, int thr, uint8_t* map, cudaStream_t s);
@@ -133,6 +164,11 @@ int vx_launch_phantom(uint8_t* dst, int64_t row_pitch, int64_t plane_pitch, int6
                       double noise_sigma, uint64_t noise_seed, const int64_t* spot_idx,
                       int64_t n_spots, int32_t spot_intensity, cudaStream_t s);
 int vx_preload_render_kernels();
+// K4 into device outputs that may live in another rank's memory (peer /
+// IPC-mapped): sys_atomics selects system-scope counter atomics
+int vx_render_tiles(vx_volume* vol, const vx_ray_setup* rs, const vx_render_params* rp,
+                    const vx_filter_config* fc, const vx_partition* part, vx_render_out* dev_out,
+                    cudaStream_t s, bool sys_atomics);
 int vx_volume_alloc(int64_t nx, int64_t ny, int64_t nz, vx_volume** out);
 int vx_volume_finish(vx_volume* v, const uint8_t* compact_dev, cudaStream_t s);
 

@@ -127,7 +127,18 @@ struct OutD {
   unsigned long long* samples;
   unsigned long long* diag;
   int32_t* trunc_flag;
+  // outputs live in another rank's memory (vx_group): system-scope atomics
+  int sys;
 };
+
+// counter update of K4's fused outputs (device scope, or system scope when
+// several GPUs accumulate into one rank's counters over NVLink)
+__device__ __forceinline__ void out_add(unsigned long long* p, unsigned long long v, int sys) {
+  if (sys)
+    atomicAdd_system(p, v);
+  else
+    atomicAdd(p, v);
+}
 
 struct RenderArgs {
   VolView V;
@@ -1243,7 +1254,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
     // unbudgeted march: only a hit at or beyond the ray's own budget can
     // differ from the budgeted reference -> exact re-render by the host
     if (!BUDGET && a.O.trunc_flag && ((hit && hidx >= limit) || st == kExhausted))
-      atomicOr(a.O.trunc_flag, 1);
+      a.O.sys ? atomicOr_system(a.O.trunc_flag, 1) : atomicOr(a.O.trunc_flag, 1);
   }
   if (valid) {
     const size_t p = (size_t)j * a.C.W + i;
@@ -1274,11 +1285,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
   // warp-level aggregation (no block barrier: warps retire independently)
   const unsigned lane = tid & 31u;
   const unsigned hits = __ballot_sync(0xffffffffu, hit);
-  if (lane == 0 && a.O.hit_count && hits) atomicAdd(a.O.hit_count, (unsigned long long)__popc(hits));
+  if (lane == 0 && a.O.hit_count && hits) out_add(a.O.hit_count, (unsigned long long)__popc(hits), a.O.sys);
   if (a.O.samples) {
     unsigned s = nsamp;
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0 && s) atomicAdd(a.O.samples, (unsigned long long)s);
+    if (lane == 0 && s) out_add(a.O.samples, (unsigned long long)s, a.O.sys);
   }
   if (DIAG) {
     for (int i = 0; i < 8; ++i) {
@@ -1323,7 +1334,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
     const unsigned key = valid ? (unsigned)pix_out : 0x100u;
     const unsigned peers = __match_any_sync(0xffffffffu, key);
     if (valid && (__ffs(peers) - 1) == (int)lane)
-      atomicAdd(a.O.image_hist + pix_out, (unsigned long long)__popc(peers));
+      out_add(a.O.image_hist + pix_out, (unsigned long long)__popc(peers), a.O.sys);
   }
 }
 
@@ -1857,8 +1868,9 @@ static double trace_us() {
 // in a small LRU on the volume.  VOXB200_ACCEPT_MAP=0 disables it, =eager
 // builds on first sight.
 static int get_accept_map(vx_volume* v, const RenderArgs& a, bool checked, const uint8_t** out,
-                          cudaStream_t s) {
+                          MapSlot** slot_out, cudaStream_t s) {
   *out = nullptr;
+  *slot_out = nullptr;
   static const int mode = [] {
     const char* e = getenv("VOXB200_ACCEPT_MAP");
     if (!e) return 1;
@@ -1891,19 +1903,24 @@ static int get_accept_map(vx_volume* v, const RenderArgs& a, bool checked, const
     if (c.valid && !memcmp(c.key, &key, sizeof(key))) e = &c;
   if (e && e->built) {
     e->stamp = v->stamp;
+    int rc = vx_map_pin(e, s);
+    if (rc) return rc;
     *out = e->map;
+    *slot_out = e;
     return VX_OK;
   }
   if (!e) {
-    e = &v->acc[0];
     for (auto& c : v->acc) {
+      if (c.pins) continue;  // a render between lookup and launch still reads it
       if (!c.valid) {
         e = &c;
         break;
       }
-      if (c.stamp < e->stamp) e = &c;
+      if (!e || c.stamp < e->stamp) e = &c;
     }
-    if (e->valid && e->built) VX_CUDA(cudaDeviceSynchronize());  // another stream may read it
+    if (!e) return VX_OK;  // every slot in flight: the raw candidate map
+    // the slot's old map is overwritten only after its last readers
+    // (vx_map_claim below orders the build after their use events)
     e->valid = true;
     e->built = false;
     memcpy(e->key, &key, sizeof(key));
@@ -1912,7 +1929,9 @@ static int get_accept_map(vx_volume* v, const RenderArgs& a, bool checked, const
   }
   double tt = trace_on() ? trace_us() : 0.0;
   e->valid = false;  // until built
-  uint8_t* occ = v->scratch;  // the volume's build scratch (held under v->mu)
+  int rc = vx_map_claim(v, e, s);
+  if (rc) return rc;
+  uint8_t* occ = v->scratch;  // the volume's build scratch (claimed above)
   VX_CUDA(cudaMemsetAsync(occ, 0, v->cmap_bytes, s));
   VX_CUDA(cudaMemsetAsync(e->map, 0, v->map_bytes, s));  // coarse level unused: no skip
   VX_TRACE("  acc scratch", tt);
@@ -1935,18 +1954,29 @@ static int get_accept_map(vx_volume* v, const RenderArgs& a, bool checked, const
   else
     dispatch_accept<false>(a.V, a.F, A, L, grid, s);
   VX_CHECK_LAUNCH();
-  int rc = vx_launch_dist_cells(v, occ, e->map + v->map_bytes, 1, s);
+  rc = vx_launch_dist_cells(v, occ, e->map + v->map_bytes, 1, s);
   if (rc) return rc;
   VX_TRACE("  acc launches", tt);
-  // other streams may pick this map up: make it visible before publishing
-  VX_CUDA(cudaStreamSynchronize(s));
-  VX_TRACE("  acc sync", tt);
+  // other streams wait on the slot's ready event (no host sync under mu)
+  if ((rc = vx_map_publish(v, e, s))) return rc;
+  if ((rc = vx_map_pin(e, s))) return rc;
   e->valid = true;
   e->built = true;
   e->stamp = v->stamp;
   *out = e->map;
+  *slot_out = e;
   return VX_OK;
 }
+
+// unpins a cached map slot when the render that looked it up returns (its
+// K4 is enqueued by then, or it failed)
+struct SlotPin {
+  vx_volume* v;
+  cudaStream_t s;
+  MapSlot* m = nullptr;
+  SlotPin(vx_volume* vol, cudaStream_t st) : v(vol), s(st) {}
+  ~SlotPin() { vx_map_release(v, m, s); }
+};
 
 // ===========================================================================
 // exported entry points
@@ -2106,7 +2136,8 @@ static int order_tiles(const OrderJob& j, cudaStream_t s) {
 
 static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_params* rp,
                        const vx_filter_config* fc, const vx_partition* part, vx_render_out* o,
-                       cudaStream_t s, int explicit_budget_override, OrderJob* defer = nullptr) {
+                       cudaStream_t s, int explicit_budget_override, OrderJob* defer = nullptr,
+                       bool sys_atomics = false) {
   if (!vol || !rs || !rp || !fc || !o || !o->pixels) {
     vx_set_error("vx_render: null argument");
     return VX_EINVAL;
@@ -2136,14 +2167,18 @@ static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_p
   const bool checked = filter_reach(a.F) > VX_PAD - 1;
   const uint8_t* dist = nullptr;
   double tt = trace_on() ? trace_us() : 0.0;
+  SlotPin pin(vol, s);  // released when this function returns (after the K4 launch)
   if (a.M.skip) {
     a.V = vx_view(vol, nullptr);
-    rc = get_accept_map(vol, a, checked, &dist, s);
+    rc = get_accept_map(vol, a, checked, &dist, &pin.m, s);
     if (rc) return rc;
     VX_TRACE("accept_map", tt);
-    if (!dist) rc = vx_get_dist_map(vol, a.M.thr, &dist, s);
+    if (!dist) rc = vx_get_dist_map(vol, a.M.thr, &dist, &pin.m, s);
     if (rc) return rc;
     VX_TRACE("dist_map", tt);
+    // every map slot in flight (more concurrent settings than slots): no
+    // skipping for this frame (exact either way)
+    if (!dist) a.M.skip = 0;
   }
   a.V = vx_view(vol, dist);
   a.O.pixels = o->pixels;
@@ -2156,6 +2191,7 @@ static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_p
   a.O.samples = reinterpret_cast<unsigned long long*>(o->samples);
   a.O.diag = reinterpret_cast<unsigned long long*>(o->diag);
   a.O.trunc_flag = o->trunc_flag;
+  a.O.sys = sys_atomics ? 1 : 0;
   a.world = part ? part->world : 1;
   a.rank = part ? part->rank : 0;
   if (a.world < 1 || a.rank < 0 || a.rank >= a.world) {
@@ -2245,6 +2281,13 @@ extern "C" int vx_render_device(vx_volume* vol, const vx_ray_setup* rs, const vx
   return render_impl(vol, rs, rp, fc, part, dev_out, s, 0);
 }
 
+// K4 over a rank's tiles straight into another rank's frame (vx_group.cu)
+int vx_render_tiles(vx_volume* vol, const vx_ray_setup* rs, const vx_render_params* rp,
+                    const vx_filter_config* fc, const vx_partition* part, vx_render_out* dev_out,
+                    cudaStream_t s, bool sys_atomics) {
+  return render_impl(vol, rs, rp, fc, part, dev_out, s, 0, nullptr, sys_atomics);
+}
+
 // per-thread frame timing events (vx_last_render_ms)
 static thread_local cudaEvent_t tl_ev[2] = {nullptr, nullptr};
 static thread_local int tl_ev_device = -1;
@@ -2331,24 +2374,25 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
   const size_t o_small = take(256 * 8 + 3 * 8 + 8 + 64);
   // per-thread staging, kept between frames (this call synchronises before
   // returning, so the next frame on this thread may reuse it)
+  // (one per (thread, device): the stream is vx_stream()'s of that device)
   static thread_local struct Staging {
     uint8_t* p = nullptr;
     size_t cap = 0;
-    int dev = -1;
-    cudaStream_t s = nullptr;
-  } st;
+  } staging[64];
   {
     int dev = 0;
     VX_CUDA(cudaGetDevice(&dev));
-    if (!st.p || st.cap < off || st.dev != dev || st.s != s) {
-      if (st.p && st.dev == dev) VX_CUDA(cudaFreeAsync(st.p, st.s));
-      st.p = nullptr;
-      VX_CUDA(vx_malloc_async(&st.p, off, s));
-      st.cap = off;
-      st.dev = dev;
-      st.s = s;
+    Staging& sg = staging[dev & 63];
+    if (!sg.p || sg.cap < off) {
+      if (sg.p) VX_CUDA(cudaFreeAsync(sg.p, s));
+      sg.p = nullptr;
+      VX_CUDA(vx_malloc_async(&sg.p, off, s));
+      sg.cap = off;
     }
   }
+  int cur_dev = 0;
+  VX_CUDA(cudaGetDevice(&cur_dev));
+  Staging& st = staging[cur_dev & 63];
   uint8_t* base = st.p;
   VX_CUDA(cudaMemsetAsync(base + o_small, 0, 256 * 8 + 3 * 8 + 8 + 64, s));
   if (part && part->world > 1) VX_CUDA(cudaMemsetAsync(base + o_pix, 0, npx, s));
@@ -2459,9 +2503,11 @@ extern "C" int vx_march_rays(vx_volume* vol, const double* origins, const double
   rc = make_filter(fc, F);
   if (rc) return rc;
   const uint8_t* dist = nullptr;
+  SlotPin pin(vol, s);
   if (M.skip) {
-    rc = vx_get_dist_map(vol, M.thr, &dist, s);
+    rc = vx_get_dist_map(vol, M.thr, &dist, &pin.m, s);
     if (rc) return rc;
+    if (!dist) M.skip = 0;
   }
   VolView V = vx_view(vol, dist);
   // one device block: in (o,d,te,tx,ms,lut) out (hit,vox,t,val)

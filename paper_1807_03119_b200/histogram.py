@@ -2,7 +2,7 @@
 
 Mirrors histogram.py:26-133 of the reference.  The 256 counts come from the
 B200 histogram kernel (computed once when the volume replica is built); the
-Otsu argmin runs on the device in exact 256-bit integer arithmetic with the
+Otsu argmin runs on the device in exact 320-bit integer arithmetic with the
 reference's tie rule (smallest T).  The 256-element derived statistics
 (probabilities, population sigma) are evaluated on the host with numpy in the
 reference's own operation order so they are bit-identical to it.
@@ -75,7 +75,7 @@ def _as_u64_counts(counts) -> np.ndarray:
 def otsu(counts) -> int:
     """Threshold minimising the weighted intra-class variance (histogram.py:59-101).
 
-    K2 on the B200: exact rational objective per T, compared by 256-bit
+    K2 on the B200: exact rational objective per T, compared by 320-bit
     cross-multiplication; ties resolve to the smallest T.
     """
     arr = _as_u64_counts(counts)

@@ -46,7 +46,8 @@ def test_binary_targets_sm100a():
     assert "sm_100a" in out.stdout
 
 
-STRUCTS = ["vx_ray_setup", "vx_render_params", "vx_filter_config", "vx_partition", "vx_render_out"]
+STRUCTS = ["vx_ray_setup", "vx_render_params", "vx_filter_config", "vx_partition", "vx_render_out",
+           "vx_group_frame"]
 
 
 @pytest.mark.skipif(shutil.which("gcc") is None, reason="gcc missing")
@@ -84,3 +85,14 @@ def test_no_device_fails_loudly(monkeypatch):
     monkeypatch.setattr(_lib, "_device_ok", None)
     with pytest.raises(_lib.NativeError, match="no CUDA device"):
         _lib.require_device()
+
+
+def test_group_blob_size_matches_header():
+    from paper_1807_03119_b200 import _lib
+
+    m = re.search(r"#define VX_GROUP_BLOB_BYTES (\d+)", HEADER.read_text())
+    assert m and int(m.group(1)) == _lib.VX_GROUP_BLOB_BYTES
+    enum = dict(re.findall(r"(VX_GROUP_SYNC_[A-Z]+) = (-?\d+)", HEADER.read_text()))
+    assert int(enum["VX_GROUP_SYNC_AUTO"]) == _lib.VX_GROUP_SYNC_AUTO
+    assert int(enum["VX_GROUP_SYNC_DEVICE"]) == _lib.VX_GROUP_SYNC_DEVICE
+    assert int(enum["VX_GROUP_SYNC_HOST"]) == _lib.VX_GROUP_SYNC_HOST

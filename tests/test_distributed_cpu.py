@@ -81,3 +81,136 @@ def test_partition_helpers():
         spans = [slab_bounds(1000, r, world) for r in range(world)]
         assert spans[0][0] == 0 and spans[-1][1] == 1000
         assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+# --- the frame-group protocol (distributed.FrameGroup) over gloo ----------------------
+
+
+class _ShmGroup:
+    """Stand-in for csrc/vx_group.cu with the same five calls: rank 0's two
+    frame slots live in a shared file; a rank's render stores its owned
+    tiles there and adds its counters under a lock (the native group does
+    this with peer stores and system-scope atomics), using the CPU oracle
+    for the pixels."""
+
+    def __init__(self, workdir, volume, T):
+        self.dir, self.volume, self.T = workdir, volume, T
+
+    def create(self, rank, world, max_pixels):
+        self.rank, self.world, self.max_pixels = rank, world, max_pixels
+        self.frame = self.released = 0
+        return f"{self.dir}/slots.bin".encode()
+
+    def shares_device(self, group):
+        return True
+
+    def connect(self, blobs, sync):
+        import fcntl
+
+        path = blobs[: len(blobs) // self.world].decode()  # rank 0's blob: its slot file
+        if self.rank == 0:
+            np.zeros(2 * (self.max_pixels + 259 * 8), np.uint8).tofile(path)
+        import torch.distributed as dist
+
+        dist.barrier()
+        self.mm = np.memmap(path, dtype=np.uint8, mode="r+")
+        self.lock = open(path + ".lock", "w")
+        self._fcntl = fcntl
+        return sync
+
+    def _slot(self, f):
+        off = (f & 1) * (self.max_pixels + 259 * 8)
+        return self.mm[off:off + self.max_pixels], self.mm[off + self.max_pixels:
+                                                         off + self.max_pixels + 259 * 8].view(np.uint64)
+
+    def render(self, dvol, rs, rp, fc, stream):
+        from oracle import oracle as orc
+        from paper_1807_03119_b200.distributed import owned_pixel_mask
+
+        cam, W, H = rs
+        self.frame += 1
+        full = orc.render(self.volume, cam, W, H, kind="local-cluster", threshold=self.T)
+        mask = owned_pixel_mask(W, H, self.rank, self.world)
+        pix, cnt = self._slot(self.frame)
+        self._fcntl.flock(self.lock, self._fcntl.LOCK_EX)
+        flat = pix[:W * H]
+        flat[mask.reshape(-1)] = full["pixels"].reshape(-1)[mask.reshape(-1)]
+        cnt[:256] += np.bincount(full["pixels"][mask], minlength=256).astype(np.uint64)
+        cnt[256] += np.uint64(int((full["hit_voxel"][:, 0] >= 0)[mask.reshape(-1)].sum()))
+        self.mm.flush()
+        self._fcntl.flock(self.lock, self._fcntl.LOCK_UN)
+        return self.frame
+
+    def download(self, pixels, counters, stream):
+        pix, cnt = self._slot(self.released + 1)
+        pixels.reshape(-1)[:] = pix[:pixels.size]
+        counters[:259] = cnt.view(np.int64)
+
+    def release(self, stream):
+        self.released += 1
+        self._slot(self.released)[1][:] = 0
+
+    def close(self):
+        pass
+
+
+def _group_worker(rank, world, port, workdir, q):
+    import sys
+
+    sys.path.insert(0, os.getcwd())
+    import torch.distributed as dist
+
+    from oracle import oracle as orc
+    from paper_1807_03119_b200.distributed import FrameGroup
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rs = np.random.default_rng(1)
+        vol = rs.integers(0, 60, (29, 23, 31), dtype=np.uint8)
+        vol[8:20, 6:16, 9:22] = 190
+        T = float(orc.otsu(orc.hist256(vol)))
+        W, H = 43, 35
+        fg = FrameGroup(W * H, backend=_ShmGroup(workdir, vol, T))
+        assert fg.host_sync
+        ok = True
+        for k, az in enumerate((10.0, 100.0, 230.0, 300.0)):
+            pos, look = orc.orbit((31, 23, 29), azimuth_deg=az)
+            cam = orc.cam_vector(pos, look, W, H)
+            fg.render(None, (cam, W, H), None, None, 0)
+            fg.finish()
+            if rank == 0:
+                full = orc.render(vol, cam, W, H, kind="local-cluster", threshold=T)
+                pix = np.zeros((H, W), np.uint8)
+                cnt = np.zeros(266, np.int64)
+                fg.download(pix, cnt, 0)
+                fg.release(0)
+                ok &= np.array_equal(pix, full["pixels"])
+                ok &= np.array_equal(cnt[:256], np.bincount(full["pixels"].reshape(-1),
+                                                            minlength=256))
+                ok &= int(cnt[256]) == full["hit_count"]
+        q.put((rank, bool(ok), fg.frames))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_frame_group_protocol(world, tmp_path):
+    """FrameGroup over gloo: blob exchange, host-ordered frames, slot reuse
+    (four frames through two slots), rank 0's download and release."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_group_worker, args=(r, world, port, str(tmp_path), q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _ in res)
+    assert all(n == 4 for *_, n in res)

@@ -1,0 +1,137 @@
+"""Multi-rank sort-first frames on the B200.
+
+The frame group's data path -- every rank's K4 storing its tiles into rank
+0's frame slot and adding its counters there with system-scope atomics -- is
+exercised on one GPU: (1) in one process through the C-ABI (two group
+handles, the in-process peer-pointer path), (2) as two processes through
+``bench.py --gpus 2`` (CUDA-IPC mapped slot, host-ordered frames, the
+functional mode of a one-GPU box).  Frames must be bit-identical to the
+single-rank frame for any rank count, as the reference's worker bands are
+(render.py:514-541, test_render.py:242-251).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def _native(vx, volume, hist, W, H, kind):
+    from paper_1807_03119_b200.filters import native_config
+    from paper_1807_03119_b200.render import native_params, ray_setup
+
+    cam = vx.orbit_camera(volume)
+    params = vx.RenderParams(width=W, height=H, background=3)
+    cfg = vx.FilterConfig(kind=kind).resolve_threshold(hist)
+    return cam, params, cfg, ray_setup(cam, W, H), native_params(params), native_config(cfg, hist)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_group_cabi_in_process(vx, small_sphere_volume, small_sphere_histogram, world):
+    from paper_1807_03119_b200 import _lib
+    from paper_1807_03119_b200.volume import device_volume
+
+    lib = _lib.load()
+    W, H = 97, 61
+    cam, params, cfg, rs, rp, fc = _native(vx, small_sphere_volume, small_sphere_histogram, W, H,
+                                           vx.FilterKind.LOCAL_CLUSTER)
+    ref = vx.render_frame(small_sphere_volume, cam, params, cfg, small_sphere_histogram)
+    dv = device_volume(small_sphere_volume)
+    groups, blobs = [], []
+    for r in range(world):
+        g = C.c_void_p()
+        b = np.zeros(_lib.VX_GROUP_BLOB_BYTES, np.uint8)
+        _lib.call("vx_group_create", r, world, W * H, C.byref(g), _lib.ptr(b))
+        groups.append(g)
+        blobs.append(b)
+    allb = np.concatenate(blobs)
+    try:
+        # one process, one GPU: the caller orders frames (host sync)
+        for g in groups:
+            _lib.call("vx_group_connect", g, _lib.ptr(allb), _lib.VX_GROUP_SYNC_AUTO)
+            mode = C.c_int32(-9)
+            _lib.call("vx_group_info", g, C.byref(mode), None)
+            assert mode.value == _lib.VX_GROUP_SYNC_HOST
+        for frame in range(3):  # slot reuse: frames 1, 2 (two slots), 3 (slot of frame 1)
+            for r in reversed(range(world)):
+                _lib.call("vx_group_render", groups[r], dv.handle, C.byref(rs), C.byref(rp),
+                          C.byref(fc), None, None)
+            pix = np.zeros(W * H, np.uint8)
+            cnt = np.zeros(259, np.uint64)
+            _lib.call("vx_group_download", groups[0], _lib.ptr(pix), _lib.ptr(cnt), W * H, None)
+            assert np.array_equal(pix.reshape(H, W), ref.pixels), frame
+            assert int(cnt[256]) == ref.hit_count
+            assert np.array_equal(cnt[:256].astype(np.int64),
+                                  np.bincount(ref.pixels.reshape(-1), minlength=256))
+            _lib.call("vx_group_release", groups[0], None)
+        # a third unreleased frame on rank 0 is refused (two slots)
+        for _ in range(2):
+            _lib.call("vx_group_render", groups[0], dv.handle, C.byref(rs), C.byref(rp),
+                      C.byref(fc), None, None)
+        with pytest.raises(_lib.NativeError, match="still held"):
+            _lib.call("vx_group_render", groups[0], dv.handle, C.byref(rs), C.byref(rp),
+                      C.byref(fc), None, None)
+    finally:
+        _lib.call("vx_synchronize")
+        for g in groups:
+            lib.vx_group_destroy(g)
+
+
+def test_group_rejects_foreign_blobs():
+    from paper_1807_03119_b200 import _lib
+
+    lib = _lib.load()
+    a, b = C.c_void_p(), C.c_void_p()
+    ba = np.zeros(_lib.VX_GROUP_BLOB_BYTES, np.uint8)
+    bb = np.zeros(_lib.VX_GROUP_BLOB_BYTES, np.uint8)
+    _lib.call("vx_group_create", 0, 2, 1000, C.byref(a), _lib.ptr(ba))
+    _lib.call("vx_group_create", 1, 2, 999, C.byref(b), _lib.ptr(bb))  # another frame size
+    try:
+        with pytest.raises(_lib.NativeError, match="does not belong"):
+            _lib.call("vx_group_connect", a, _lib.ptr(np.concatenate([ba, bb])), -1)
+        # ranks on one GPU cannot use the device flags
+        c = C.c_void_p()
+        bc = np.zeros(_lib.VX_GROUP_BLOB_BYTES, np.uint8)
+        _lib.call("vx_group_create", 1, 2, 1000, C.byref(c), _lib.ptr(bc))
+        with pytest.raises(_lib.NativeError, match="one GPU per rank"):
+            _lib.call("vx_group_connect", a, _lib.ptr(np.concatenate([ba, bc])),
+                      _lib.VX_GROUP_SYNC_DEVICE)
+        lib.vx_group_destroy(c)
+    finally:
+        lib.vx_group_destroy(a)
+        lib.vx_group_destroy(b)
+
+
+def _bench(*args, timeout=600):
+    env = dict(os.environ, PYTHONPATH=str(ROOT))
+    res = subprocess.run([sys.executable, str(ROOT / "bench.py"), *args], capture_output=True,
+                         text=True, timeout=timeout, cwd=str(ROOT), env=env)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-4000:]
+    lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, res.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_bench_two_ranks_match_one_rank():
+    """bench.py --gpus 2 launches its two ranks itself; on a one-GPU box they
+    share the GPU (IPC-mapped frame slot, host-ordered frames).  The frame is
+    bit-identical to the single-rank frame."""
+    common = ["--size", "256", "--image", "320", "--steps", "4", "--warmup", "3", "--no-cpu",
+              "--orbit", "0", "--noskip-steps", "0", "--ncu", "off"]
+    one = _bench("--gpus", "1", *common)
+    two = _bench("--gpus", "2", *common)
+    assert one["n_gpus"] == 1 and two["n_gpus"] == 2
+    assert two["frame"]["sha256_16"] == one["frame"]["sha256_16"]
+    assert two["frame"]["hits"] == one["frame"]["hits"]
+    assert two["config"]["otsu_T"] == one["config"]["otsu_T"]
+    assert two["e2e"]["value"] > 0 and two["value"] > 0

@@ -340,7 +340,7 @@ def test_sharded_api_single_rank_nccl(vx, small_sphere_volume, small_sphere_hist
     torch.cuda.set_device(0)
     dist.init_process_group("nccl", rank=0, world_size=1)
     try:
-        h = histogram_sharded(small_sphere_volume.data)
+        h = histogram_sharded(small_sphere_volume)
         assert np.array_equal(h.counts, small_sphere_histogram.counts)
         assert h.otsu_threshold == small_sphere_histogram.otsu_threshold
         cam = vx.orbit_camera(small_sphere_volume)

@@ -145,7 +145,7 @@ def test_k2_otsu_scale_invariance_and_big_counts(vx, oracle):
         counts = [int(v) for v in rs.integers(0, 50, 256)]
         k = int(rs.integers(1, 10000))
         assert vx.otsu(counts) == vx.otsu([k * v for v in counts]) == oracle.otsu(counts)
-    # 4096^3-sized histograms: 2^36 voxels need the 256-bit compare
+    # 4096^3-sized histograms: 2^36 voxels need the 320-bit compare
     for _ in range(10):
         counts = rs.integers(0, 2 ** 28, 256)
         counts[0] = 2 ** 35
