@@ -289,6 +289,12 @@ int vx_phantom_device(uint8_t* dev_out, int64_t nx, int64_t ny, int64_t nz,
                       uint64_t noise_seed, const int64_t* spot_idx, int64_t n_spots,
                       int32_t spot_intensity, void* stream);
 
+/* C4 input generator: u16[i] = clamp(257*v8[i] + e_i, 0, 65535),
+ * e_i = (splitmix64 stream(seed) draw i0+i mod 257) - 128, so load_raw's
+ * 16-bit rescale (volume.py:148-150) returns v8 exactly.  Device buffers. */
+int vx_u16_dither_device(const uint8_t* dev_v8, uint64_t n, uint64_t i0, uint64_t seed,
+                         uint16_t* dev_out, void* stream);
+
 /* ---- pinned host memory (frame outputs DMA'd without staging) ------------ */
 int vx_host_alloc(uint64_t bytes, void** out);
 int vx_host_free(void* ptr);

@@ -159,6 +159,7 @@ SIGNATURES = {
     "vx_host_free": [P],
     "vx_volume_distance_map": [P, I32, I32, P, P],
     "vx_volume_histogram_slab": [P, I64, I64, P, P],
+    "vx_u16_dither_device": [P, U64, U64, U64, P, P],
     "vx_group_create": [I32, I32, I64, P, P],
     "vx_group_connect": [P, P, I32],
     "vx_group_info": [P, P, P],

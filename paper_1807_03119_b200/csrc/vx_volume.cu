@@ -7,6 +7,8 @@
 
 #include <cstring>
 
+#include <algorithm>
+
 #include "vx_internal.cuh"
 
 namespace {
@@ -257,7 +259,36 @@ __global__ void spot_kernel(uint8_t* __restrict__ dst, int64_t rp, int64_t pp, i
   dst[z * pp + y * rp + x] = (uint8_t)val;
 }
 
+// C4 input: a 16-bit CT file whose load_raw rescale
+// (v + 128) / 257 (volume.py:148-150) returns exactly v8 -- u16 =
+// clamp(257*v8 + e, 0, 65535) with dither e = (stream(seed)[i] mod 257) - 128
+// in [-128, 128]
+__global__ void u16_dither_kernel(const uint8_t* __restrict__ v8, uint64_t n, uint64_t i0,
+                                  unsigned long long seed, uint16_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long b = mix64(seed + (i0 + i + 1ull) * 0x9E3779B97F4A7C15ull);
+    const int e = (int)(b % 257ull) - 128;
+    int v = 257 * (int)v8[i] + e;
+    v = v < 0 ? 0 : (v > 65535 ? 65535 : v);
+    out[i] = (uint16_t)v;
+  }
+}
+
 }  // namespace
+
+extern "C" int vx_u16_dither_device(const uint8_t* dev_v8, uint64_t n, uint64_t i0, uint64_t seed,
+                                    uint16_t* dev_out, void* stream) {
+  if ((!dev_v8 || !dev_out) && n) {
+    vx_set_error("vx_u16_dither_device: null argument");
+    return VX_EINVAL;
+  }
+  if (!n) return VX_OK;
+  const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)vx_sm_count() * 16);
+  u16_dither_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(dev_v8, n, i0, seed, dev_out);
+  VX_CHECK_LAUNCH();
+  return VX_OK;
+}
 
 int vx_launch_brick_max(vx_volume* v, cudaStream_t s) {
   const int64_t nb = (int64_t)v->nbx * v->nby * v->nbz;

@@ -133,3 +133,51 @@ def insect_phantom_spec(dims: int = 512, seed: int = INSECT_PHANTOM_SEED) -> Pha
     return PhantomSpec(dims=(dims, dims, dims), shapes=tuple(shapes), noise_sigma=12.0,
                        spot_noise=SpotNoise(density=(n_spots + 0.5) / dims ** 3, intensity=255),
                        rng_seed=seed)
+
+
+CT_DITHER_SEED = 2048
+
+
+def write_ct_u16(spec, path, seed: int = CT_DITHER_SEED, chunk: int = 1 << 28) -> "VolumeMeta":
+    """The C4 input: a headerless 16-bit CT file of the
+    phantom ``spec`` plus its ``.meta.json`` sidecar, such that load_raw's
+    rescale (volume.py:148-150) returns the phantom's 8-bit voxels exactly:
+    u16 = clamp(257*v8 + e, 0, 65535), dither e in [-128, 128]
+    (vx_u16_dither_device).  Generated on the device (K7, then the dither
+    kernel) and written chunk by chunk; an input generator, not a
+    parity-bearing path."""
+    import ctypes as C
+    import json
+    from pathlib import Path
+
+    import numpy as np
+    import torch
+
+    from . import _lib
+    from .volume import VolumeMeta, _phantom_args, meta_path_for
+
+    _lib.require_device()
+    nx, ny, nz = spec.dims
+    n = nx * ny * nz
+    table, n_shapes, nseed, spots, k = _phantom_args(spec)
+    stream = torch.cuda.current_stream()
+    sp = C.c_void_p(stream.cuda_stream)
+    v8 = torch.empty(n, dtype=torch.uint8, device="cuda")
+    _lib.call("vx_phantom_device", C.c_void_p(v8.data_ptr()), nx, ny, nz, _lib.ptr(table),
+              n_shapes, float(spec.noise_sigma), nseed, _lib.ptr(spots), k,
+              int(spec.spot_noise.intensity), sp)
+    wide = torch.empty(min(chunk, n), dtype=torch.int16, device="cuda")
+    host = torch.empty(min(chunk, n), dtype=torch.int16, pin_memory=True)
+    path = Path(path)
+    with open(path, "wb") as f:
+        for i0 in range(0, n, chunk):
+            m = min(chunk, n - i0)
+            _lib.call("vx_u16_dither_device", C.c_void_p(v8.data_ptr() + i0), m, i0, seed,
+                      C.c_void_p(wide.data_ptr()), sp)
+            host[:m].copy_(wide[:m])
+            torch.cuda.synchronize()
+            f.write(memoryview(host[:m].numpy().view(np.uint8)))
+    del v8, wide, host
+    meta = VolumeMeta(dims=spec.dims, bit_depth=16, source="write_ct_u16")
+    meta_path_for(path).write_text(json.dumps(meta.to_json()))
+    return meta
