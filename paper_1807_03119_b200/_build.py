@@ -13,6 +13,9 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libvoxb200.so"
+# bounds-checked, schedule-jittered variant (tests/test_gpu_checked.py; the
+# stand-in for compute-sanitizer, which is closed on this pool)
+CHECKED_LIB = PKG / "libvoxb200_checked.so"
 INCLUDE = PKG.parent / "include"
 
 SOURCES = ["vx_api.cu", "vx_hist.cu", "vx_volume.cu", "vx_render.cu", "vx_io.cu", "vx_group.cu"]
@@ -34,30 +37,32 @@ def nvcc() -> str:
     return cand if Path(cand).exists() else "nvcc"
 
 
-def needs_build() -> bool:
-    if not LIB.exists():
+def needs_build(lib: Path = LIB) -> bool:
+    if not lib.exists():
         return True
-    mtime = LIB.stat().st_mtime
+    mtime = lib.stat().st_mtime
     deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h"))
     return any(p.stat().st_mtime > mtime for p in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
-    if not force and not needs_build():
-        return LIB
+def build(verbose: bool = False, force: bool = False, checked: bool = False) -> Path:
+    lib = CHECKED_LIB if checked else LIB
+    if not force and not needs_build(lib):
+        return lib
     cmd = [nvcc(), *NVCC_FLAGS, "-I", str(INCLUDE)]
+    if checked:
+        cmd += ["-DVX_DEBUG_CHECKS", "-DVX_DEBUG_JITTER"]
     if verbose:
         cmd += ["-Xptxas", "-v"]
-    cmd += [str(CSRC / s) for s in SOURCES] + ["-o", str(LIB) + ".tmp"]
+    cmd += [str(CSRC / s) for s in SOURCES] + ["-o", str(lib) + ".tmp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)
     if verbose:
         sys.stderr.write(res.stdout + res.stderr)
-    os.replace(str(LIB) + ".tmp", LIB)
-    return LIB
+    os.replace(str(lib) + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(verbose="--verbose" in sys.argv, force=True)
-    print(LIB)
+    print(build(verbose="--verbose" in sys.argv, force=True, checked="--checked" in sys.argv))

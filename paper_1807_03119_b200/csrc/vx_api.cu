@@ -127,6 +127,12 @@ VolView vx_view(const vx_volume* v, const uint8_t* dist_map) {
   V.csy = v->csy;
   V.csz = v->csz;
   V.dist2 = dist_map ? dist_map + v->map_bytes + v->csz + v->csy + 1 : nullptr;
+#ifdef VX_DEBUG_CHECKS
+  V.lo = v->alloc;
+  V.hi = v->alloc + v->alloc_bytes;
+  V.d2lo = dist_map ? dist_map + v->map_bytes : nullptr;
+  V.d2hi = dist_map ? dist_map + v->map_bytes + v->cmap_bytes : nullptr;
+#endif
   return V;
 }
 

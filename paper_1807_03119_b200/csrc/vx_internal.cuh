@@ -57,7 +57,31 @@ struct VolView {
   int64_t bsy, bsz;       // strides of the brick maps
   const uint8_t* dist2;   // Chebyshev cell-distance map at cell (0,0,0)
   int64_t csy, csz;       // strides of the cell maps
+#ifdef VX_DEBUG_CHECKS
+  // bounds of the padded allocation and of the cell map (checked build only)
+  const uint8_t *lo, *hi, *d2lo, *d2hi;
+#endif
 };
+
+// Checked build (-DVX_DEBUG_CHECKS, libvoxb200_checked.so): every voxel read
+// must stay inside the zero apron (|overshoot| <= VX_PAD) and the allocation,
+// every map read inside its map, every shared-scratch index inside its
+// array; a violation prints the kernel's coordinates and traps (the stand-in
+// for compute-sanitizer memcheck, which is closed on this pool).
+#ifdef VX_DEBUG_CHECKS
+#define VX_DCHECK(cond, fmt, ...)                                                      \
+  do {                                                                                 \
+    if (!(cond)) {                                                                     \
+      printf("VX_DCHECK %s:%d block %d thread %d: " fmt "\n", __FILE__, __LINE__,       \
+             (int)blockIdx.x, (int)(threadIdx.y * blockDim.x + threadIdx.x), __VA_ARGS__); \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define VX_DCHECK(cond, fmt, ...) \
+  do {                            \
+  } while (0)
+#endif
 
 // Lifetime of a cached map slot (distance or accepted-cell map).  A render
 // pins the slot from its lookup until its K4 is enqueued, then records the

@@ -176,6 +176,13 @@ __device__ __forceinline__ int rd(const VolView& V, long long x, long long y, lo
   if (CHECKED) {
     if (x < 0 || y < 0 || z < 0 || x >= V.nx || y >= V.ny || z >= V.nz) return 0;
   }
+  VX_DCHECK(x >= -VX_PAD && y >= -VX_PAD && z >= -VX_PAD && x < V.nx + VX_PAD &&
+                y < V.ny + VX_PAD && z < V.nz + VX_PAD,
+            "voxel (%lld, %lld, %lld) outside the apron of (%d, %d, %d)", x, y, z, V.nx, V.ny,
+            V.nz);
+  VX_DCHECK(V.origin + (z * V.sz + y * V.sy + x) >= V.lo &&
+                V.origin + (z * V.sz + y * V.sy + x) < V.hi,
+            "voxel (%lld, %lld, %lld) outside the allocation", x, y, z);
   return __ldg(V.origin + (z * V.sz + y * V.sy + x));
 }
 
@@ -618,7 +625,16 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
   // stop > 0 (a split ray's first segment): hand over at sample `stop`
   int guard = BUDGET ? limit : (limit > (1 << 30) ? INT_MAX : limit + (1 << 20));
   if (!BUDGET && stop > 0 && stop < guard) guard = stop;
+#ifdef VX_DEBUG_JITTER
+  unsigned jit = lane * 2654435761u + blockIdx.x * 40503u;
+#endif
   while (__any_sync(0xffffffffu, status == kRunning)) {
+#ifdef VX_DEBUG_JITTER
+    // checked build: lanes sleep 0-2 us at random before every step, so a
+    // shared-scratch access missing its __syncwarp shows as a wrong frame
+    jit = jit * 1664525u + 1013904223u;
+    if (jit & 0x10000u) __nanosleep((jit >> 21) & 2047u);
+#endif
     bool need = false;
     int m = chunk;
     if (status == kRunning) {
@@ -658,6 +674,9 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
           const int cx = vx >> VX_CELL_SHIFT, cy = vy >> VX_CELL_SHIFT, cz = vz >> VX_CELL_SHIFT;
           // in-span samples truncate into [0, n]: inside the map's 1-cell apron
           VX_DIAG(dLookup);
+          VX_DCHECK(V.dist2 + (cz * (int)V.csz + cy * (int)V.csy + cx) >= V.d2lo &&
+                        V.dist2 + (cz * (int)V.csz + cy * (int)V.csy + cx) < V.d2hi,
+                    "cell (%d, %d, %d) outside the distance map", cx, cy, cz);
           const int D = __ldg(V.dist2 + (cz * (int)V.csz + cy * (int)V.csy + cx));
           float lim = -1.0f;
           if (D >= M.skip_min_d) {
@@ -970,6 +989,7 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
           while (c) {
             const int j = __ffs(c) - 1;
             c &= c - 1;
+            VX_DCHECK(off + i < 256, "candidate item %d outside the warp scratch", off + i);
             ws->items[off + i++] = (unsigned char)((lane << 3) | j);
           }
         }
@@ -997,6 +1017,7 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
             VX_DIAG(dFilter);
             const double f = filter_value<KIND, CHECKED>(V, F, lut, __float2int_rz(px),
                                                          __float2int_rz(py), __float2int_rz(pz));
+            VX_DCHECK(w < 256, "pass slot %d outside the warp scratch", w);
             ws->pass[w] = f >= M.T ? 1 : 0;
           }
         }
@@ -1258,6 +1279,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
   }
   if (valid) {
     const size_t p = (size_t)j * a.C.W + i;
+    VX_DCHECK(i >= 0 && j >= 0 && i < a.C.W && j < a.C.H, "pixel (%d, %d) outside the frame", i, j);
     uint8_t pix = (uint8_t)a.S.background;
     double I = -1.0;
     if (hit) {

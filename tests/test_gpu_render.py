@@ -445,3 +445,46 @@ def test_concurrent_render_frame_threads(vx):
     for (i, rep), px in got.items():
         assert np.array_equal(px, want[i]), (i, rep)
     assert len(got) == len(jobs) * 4
+
+
+def test_map_cache_eviction_stress_threads(vx):
+    """Six threads x six filter settings on one shared volume: more distinct
+    thresholds (candidate distance maps) and filter settings (accepted-cell
+    maps) than the volume's 4 + 4 cached map slots, so maps are evicted and
+    rebuilt while other threads' frames are in flight.  A slot is pinned
+    from lookup to K4 launch and rebuilt only after its readers (per-stream
+    use events), so every frame equals its single-threaded render."""
+    import threading
+
+    from oracle.rng_np import generate_phantom_np
+    from paper_1807_03119_b200 import phantoms
+
+    spec = phantoms.spot_phantom_spec(64)
+    v = vx.Volume(dims=spec.dims, data=generate_phantom_np(spec.to_json()))
+    h = vx.build_histogram(v)
+    kinds = [vx.FilterKind.LOCAL_CLUSTER, vx.FilterKind.MEAN, vx.FilterKind.SIGMA]
+    settings = [vx.FilterConfig(kind=kinds[i % 3], threshold=float(t))
+                for i, t in enumerate((30, 46, 61, 80, 101, 125))]
+    params = vx.RenderParams(width=320, height=300)
+    cams = [vx.orbit_camera(v, azimuth_deg=17.0 * w, elevation_deg=5.0 + 6 * w) for w in range(6)]
+    want = {(w, s): vx.render_frame(v, cams[w], params, settings[s], h).pixels.copy()
+            for w in range(6) for s in range(6)}
+    bad, errors = [], []
+
+    def worker(w):
+        try:
+            order = np.random.default_rng(w).permutation(6 * 5) % 6
+            for s in order:
+                px = vx.render_frame(v, cams[w], params, settings[s], h).pixels
+                if not np.array_equal(px, want[(w, s)]):
+                    bad.append((w, int(s)))
+        except Exception as exc:  # surfaced below
+            errors.append(exc)
+
+    ts = [threading.Thread(target=worker, args=(w,)) for w in range(6)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    assert not bad, bad
