@@ -263,11 +263,18 @@ class PinnedPool:
     A buffer returns to the pool when the last array viewing it is freed."""
 
     ARENA_BYTES = 16 << 20  # two 2048^2 frames with counters, or many smaller ones
+    MAX_FRAME_SIZES = 8  # frame-size entries kept (LRU); older sizes are dropped
+    FREE_CAP = 64 << 20  # page-locked bytes parked for reuse beyond the arena
 
     def __init__(self):
+        from collections import OrderedDict
+
         self._free: dict[int, list[int]] = {}
-        self._frames: dict[tuple[int, int], list[list]] = {}
-        self._lock = threading.Lock()
+        self._free_bytes = 0
+        self._frames: OrderedDict = OrderedDict()
+        # re-entrant: buffer finalizers (_release) can run inside a locked
+        # region when dropping an entry frees the last reference
+        self._lock = threading.RLock()
         self._arena = 0  # page-locked block new buffers are carved from
         self._arena_left = 0
 
@@ -309,6 +316,8 @@ class PinnedPool:
         with self._lock:
             lst = self._free.get(nbytes)
             ptr = lst.pop() if lst else None
+            if ptr is not None and not self._in_arena(ptr):
+                self._free_bytes -= nbytes
         if ptr is None:
             ptr = self._carve(nbytes)
         if ptr is None:
@@ -324,8 +333,21 @@ class PinnedPool:
         weakref.finalize(buf, self._release, nbytes, ptr)
         return np.frombuffer(buf, dtype=dtype, count=count).reshape(shape), ptr
 
+    def _in_arena(self, ptr) -> bool:
+        return bool(self._arena) and self._arena <= ptr < self._arena + self.ARENA_BYTES
+
     def _release(self, nbytes, ptr):
         with self._lock:
+            if not self._in_arena(ptr):
+                if self._free_bytes + nbytes > self.FREE_CAP:
+                    # bounded: a viewer resizing its window does not pin
+                    # host memory without limit
+                    try:
+                        call("vx_host_free", C.c_void_p(ptr))
+                    except NativeError:
+                        pass
+                    return
+                self._free_bytes += nbytes
             self._free.setdefault(nbytes, []).append(ptr)
 
     def frame(self, height: int, width: int) -> tuple[np.ndarray, np.ndarray, int, int]:
@@ -337,6 +359,11 @@ class PinnedPool:
         key = (height, width)
         with self._lock:
             lst = self._frames.setdefault(key, [])
+            self._frames.move_to_end(key)
+            # LRU over frame sizes: a dropped size's buffers go back to the
+            # size-keyed free list (or are freed) when their arrays die
+            while len(self._frames) > self.MAX_FRAME_SIZES:
+                self._frames.popitem(last=False)
             for ent in lst:
                 # free when only the entry references its arrays and its
                 # buffer: numpy views of views may point at either the view or
@@ -361,7 +388,7 @@ class PinnedPool:
             made.append(ent)
         pix, small, p0, p1 = made[0][:4]
         with self._lock:
-            self._frames[key].extend(made)
+            self._frames.setdefault(key, []).extend(made)
         return pix, small, p0, p1
 
 

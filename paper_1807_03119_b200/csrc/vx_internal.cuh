@@ -133,7 +133,7 @@ struct vx_volume {
   int nbx, nby, nbz;
   int64_t bsy, bsz;
   uint64_t map_bytes;
-  // cell (2^3) max map with a 1-cell apron: dims (ncx+2, ncy+2, ncz+2)
+  // cell (4^3) max map with a 1-cell apron: dims (ncx+2, ncy+2, ncz+2)
   uint8_t* cmax;
   int ncx, ncy, ncz;
   int64_t csy, csz;

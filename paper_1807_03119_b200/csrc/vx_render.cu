@@ -12,16 +12,22 @@
 //   * integer filter sums, FP64 quotient                     filters.py:165-227
 //   * exact-integer Sobel gradient, FP64 normal + Phong       render.py:344-403
 //
-// Exact empty-space skipping: a sample can only become a surface candidate
-// when raw >= thr = ceil(T) (render.py:258,307).  The volume carries an 8^3
-// brick-max map; per thr we build the Chebyshev brick distance D to the
-// nearest brick whose max reaches thr.  At the start of a chunk, if the
-// chunk's first sample lies in a brick with D >= 2, every sample whose t is
-// within 8(D-1) - 1/16 voxel of it lies in bricks of max < thr (its
-// truncated voxel is within D-1 bricks; FP32 rounding of the positions is
-// < 2^-7 voxel for volumes up to 8192^3), so those chunks are advanced with
-// the exact FP32 base recurrence and never sampled.  Result-neutral by
-// construction; disabled automatically when thr == 0 (every brick occupied).
+// Exact empty-space skipping: a sample can only become a
+// surface candidate when raw >= thr = ceil(T) (render.py:258,307), and only
+// an accepted candidate (f >= T) ends a ray (render.py:311-329).  Per thr
+// (and per filter setting) the volume keeps a map of 4^3 cells holding the
+// Chebyshev cell distance D (capped at 32) to the nearest cell with a
+// candidate-level voxel (the candidate map) or with an accepted voxel (the
+// accepted-cell map, K8).  At a sample in a cell with D >= skip_min_d (2 for
+// step >= 0.5, else 1), every cell within distance D-1 is empty, so every
+// later sample whose t lies before the ray's exit from that box -- its far
+// faces shrunk by 1/8 voxel, less a t margin of 1/16 + |t| 2^-19 -- truncates
+// into an empty cell (computed positions are monotone in t and their FP32
+// error is < 2^-7 voxel for |p|, |t| < 8192).  Those samples are stepped
+// over by index inside a chunk and by the exact FP32 base recurrence across
+// chunks, so the t of every sample actually taken is bit-identical to the
+// reference's.  Result-neutral by construction; switched off when thr == 0
+// (every cell occupied).
 
 #include <atomic>
 #include <chrono>

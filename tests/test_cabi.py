@@ -96,3 +96,20 @@ def test_group_blob_size_matches_header():
     assert int(enum["VX_GROUP_SYNC_AUTO"]) == _lib.VX_GROUP_SYNC_AUTO
     assert int(enum["VX_GROUP_SYNC_DEVICE"]) == _lib.VX_GROUP_SYNC_DEVICE
     assert int(enum["VX_GROUP_SYNC_HOST"]) == _lib.VX_GROUP_SYNC_HOST
+
+
+def test_checked_variant_carries_the_checks():
+    """libvoxb200_checked.so (the compute-sanitizer stand-in run by
+    tests/test_gpu_checked.py) really contains the bounds traps and the
+    schedule jitter; the production library contains neither."""
+    from paper_1807_03119_b200 import _build
+
+    checked = _build.build(checked=True)
+    cob = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+
+    def sass(p):
+        return subprocess.run([cob, "-sass", str(p)], capture_output=True, text=True).stdout
+
+    s_checked, s_prod = sass(checked), sass(_build.LIB)
+    assert s_checked.count("BPT.TRAP") > 100 and "NANOSLEEP" in s_checked
+    assert "BPT.TRAP" not in s_prod and "NANOSLEEP" not in s_prod

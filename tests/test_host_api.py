@@ -272,3 +272,36 @@ def test_pinned_arena_serves_first_frames(monkeypatch):
     assert hi - lo >= 1024 * 1024 + 266 * 8
     big = pool.array((pool.ARENA_BYTES,), np.uint8)  # does not fit the rest: allocated
     assert len(allocs) == 3 and big.size == pool.ARENA_BYTES
+
+
+def test_pinned_pool_is_bounded(monkeypatch):
+    """A client that keeps changing its frame size does not grow page-locked
+    memory without bound: at most MAX_FRAME_SIZES sizes keep entries, and
+    parked buffers beyond FREE_CAP are freed."""
+    import ctypes as C
+    import gc
+
+    from paper_1807_03119_b200 import _lib
+
+    keep, allocs, freed = {}, [], []
+
+    def fake_call(name, *args, **kw):
+        if name == "vx_host_free":
+            freed.append(args[0].value)
+            return
+        assert name == "vx_host_alloc"
+        b = (C.c_uint8 * args[0])()
+        keep[C.addressof(b)] = b
+        allocs.append(args[0])
+        args[1]._obj.value = C.addressof(b)
+
+    monkeypatch.setattr(_lib, "call", fake_call)
+    pool = _lib.PinnedPool()
+    monkeypatch.setattr(pool, "FREE_CAP", 1 << 20)
+    for w in range(40, 80):  # 40 distinct sizes, frames dropped right away
+        f = pool.frame(512, w)
+        del f
+        gc.collect()
+    assert len(pool._frames) <= pool.MAX_FRAME_SIZES
+    assert pool._free_bytes <= pool.FREE_CAP
+    assert freed  # the overflow went back to the driver
