@@ -61,9 +61,10 @@ sys.path.insert(0, str(ROOT))
 METRIC = "filtered frames/s (ms/frame) at 1024² on 1024³ CT; Otsu hist GB/s vs HBM"
 
 
-def workload_name(size: int, image: int, filt: str) -> str:
+def workload_name(size: int, image: int, filt: str, u16: bool = False) -> str:
     """The config.workload string both arms print (identical for one config)."""
-    return (f"insect_{size}^3 (C2 recipe x{size / 512:g}, device-generated uint8) @ "
+    src = "uint16 CT file" if u16 else "uint8"
+    return (f"insect_{size}^3 (C2 recipe x{size / 512:g}, {src}) @ "
             f"{image}x{image}, {filt}, Otsu T")
 
 
@@ -85,6 +86,11 @@ def parse(argv=None):
     ap.add_argument("--ncu", default="auto", choices=["auto", "on", "off"],
                     help="DRAM traffic pass under ncu (auto: when ncu is on PATH and N=1)")
     ap.add_argument("--ncu-child", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--no-python-ref", dest="python_ref", action="store_false",
+                    help="reference arm: skip timing the Python reference at C2")
+    ap.add_argument("--u16", action="store_true",
+                    help="C4 input: write the phantom as a 16-bit CT file and ingest it "
+                         "through load_raw (rank 0), instead of generating it in HBM")
     ap.add_argument("--sync", default="auto", choices=["auto", "device", "host"],
                     help="N>1 frame ordering (auto: device flags unless ranks share a GPU)")
     return ap.parse_args(argv)
@@ -220,6 +226,41 @@ def sha16(a: np.ndarray) -> str:
 # ------------------------------------------------------------------------------------
 
 
+def python_reference_c2(threads: int) -> dict:
+    """The unmodified Python reference (baseline/_ref, scripts/install_reference.sh)
+    timed on this host at BASELINE.json C2 (insect 512^3 @1024^2, local
+    cluster): render_frame with 1 worker and with every host thread.  A stated
+    baseline beside the arm's C port of the same path."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "voxray" / "render.py").exists():
+        return {"status": "baseline/_ref not installed"}
+    sys.path.insert(0, str(ref))
+    try:
+        import voxray
+        from oracle import oracle as orc
+
+        from paper_1807_03119_b200 import phantoms  # the spec constants only (dataclasses)
+
+        data = orc.phantom(phantoms.insect_phantom_spec(512).to_json(), threads=threads)
+        vol = voxray.Volume(dims=(512, 512, 512), data=data)
+        hist = voxray.build_histogram(vol)
+        cam = voxray.orbit_camera(vol)
+        params = voxray.RenderParams(width=1024, height=1024)
+        cfg = voxray.FilterConfig(kind=voxray.FilterKind.LOCAL_CLUSTER)
+        out = {"status": "ok", "config": "C2: insect_512^3 @ 1024x1024, local-cluster, Otsu T",
+               "module": voxray.__file__, "otsu_T": int(hist.otsu_threshold)}
+        for workers in (1, threads):
+            t0 = time.perf_counter()
+            f = voxray.render_frame(vol, cam, params, cfg, hist, workers=workers)
+            out[f"frame_s_workers_{workers}"] = time.perf_counter() - t0
+        out["frame_sha256_16"] = sha16(f.pixels)
+        return out
+    except Exception as exc:  # reported, never fatal for the arm
+        return {"status": f"failed: {exc!r}"[:300]}
+    finally:
+        sys.path.remove(str(ref))
+
+
 def run_reference(args):
     """--impl reference: the reference's CPU path (the oracle C restatement,
     oracle/vxoracle.c, pinned to the live reference's frames) on every host
@@ -258,7 +299,7 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": per_frame * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": workload_name(args.size, args.image, args.filter),
+        "config": {"workload": workload_name(args.size, args.image, args.filter, args.u16),
                    "volume": [args.size] * 3, "image": [W, H], "filter": args.filter,
                    "otsu_T": hm["otsu"]},
         "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "port",
@@ -268,6 +309,7 @@ def run_reference(args):
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "frame": {"sha256_16": sha16(pixels), "otsu_T": hm["otsu"]},
+        "python_reference": python_reference_c2(threads) if args.python_ref else None,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -351,7 +393,8 @@ def run_ours(args):
     from paper_1807_03119_b200.filters import native_config
     from paper_1807_03119_b200.histogram import model_from_counts
     from paper_1807_03119_b200.render import native_params, ray_setup
-    from paper_1807_03119_b200.volume import _attach, _phantom_args, generate_phantom_device
+    from paper_1807_03119_b200.volume import (_attach, _phantom_args, device_volume,
+                                              generate_phantom_device)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -378,7 +421,33 @@ def run_ours(args):
 
     # ---- workload: every rank holds the full volume (sort-first) ----
     t0 = time.perf_counter()
-    if world == 1:
+    volume = None  # host Volume (rank 0), when the workload has one
+    ingest = None
+    if args.u16:
+        # C4 as BASELINE.json states it: a uint16 CT file through load_raw's
+        # streamed device path (volume.py:122-151) on the source rank
+        if rank == 0:
+            tmp = Path(os.environ.get("TMPDIR", "/tmp")) / f"vx_ct{args.size}_{os.getpid()}.raw"
+            phantoms.write_ct_u16(spec, tmp)
+            torch.cuda.synchronize()
+            ti = time.perf_counter()
+            volume = vx.load_raw(tmp)
+            ingest_s = time.perf_counter() - ti
+            ingest = {"file_bytes": 2 * nvox, "seconds": ingest_s,
+                      "gbs": 2 * nvox / ingest_s / 1e9,
+                      "path": "load_raw -> vx_volume_load_raw (pread slots overlapped with H2D, "
+                              "u16 rescale on the device)"}
+            tmp.unlink()
+            Path(str(tmp)[:-4] + ".meta.json").unlink()
+        if world == 1:
+            dvol = device_volume(volume)
+            counts = dvol.counts()
+            hist = model_from_counts(counts)
+        else:
+            dvol = distributed.replicate_volume(spec.dims, volume=volume)  # NCCL broadcast
+            hist = distributed.histogram_sharded(dvol)
+            counts = hist.counts
+    elif world == 1:
         dvol = generate_phantom_device(spec)
         counts = dvol.counts()
         hist = model_from_counts(counts)  # K1 (at creation) + K2
@@ -393,8 +462,8 @@ def run_ours(args):
         dvol = distributed.replicate_volume(spec.dims, fill=fill)  # NCCL broadcast
         hist = distributed.histogram_sharded(dvol)  # z-slab K1 + all-reduce + K2
         counts = hist.counts
-        if not np.array_equal(counts, dvol.counts()):
-            raise SystemExit("sharded histogram differs from the replica's own K1")
+    if world > 1 and not np.array_equal(counts, dvol.counts()):
+        raise SystemExit("sharded histogram differs from the replica's own K1")
     gen_s = time.perf_counter() - t0
 
     cfg = vx.FilterConfig(kind=vx.FilterKind.from_name(args.filter)).resolve_threshold(hist)
@@ -524,13 +593,43 @@ def run_ours(args):
                                "tile order, frame 2 builds the filter's accepted-cell map; timed "
                                "frames reuse both (per volume/setting caches)"}
 
+    # ---- march statistics of the frame: the dependent-lookup latency model ----
+    lat_model = None
+    if world == 1:
+        diag = torch.zeros(8, dtype=torch.int64, device="cuda")
+        small.zero_()
+        out.diag = diag.data_ptr()
+        _lib.call("vx_render_device", dvol.handle, C.byref(rs), C.byref(rp), C.byref(fc), None,
+                  C.byref(out), sptr)
+        torch.cuda.synchronize()
+        out.diag = None
+        dg = dict(zip(("lookups", "skips", "chunks_skipped", "unused", "sample_groups",
+                       "filter_evals", "hits", "iterations"), diag.cpu().tolist()))
+        rays = W * H
+        sm_count = torch.cuda.get_device_properties(dev_index).multi_processor_count
+        clk = (clocks.summary().get("sm_mhz") or 1965.0) * 1e6
+        l2_cycles = 248.0  # B300_MICROARCH.md: L2 hit 234 (near die) / 262 (far die)
+        warp_steps = dg["iterations"] / 32.0
+        model_ms = warp_steps * l2_cycles / clk / (sm_count * 32) * 1e3
+        lat_model = {
+            **dg, "rays": rays,
+            "iterations_per_ray": dg["iterations"] / rays,
+            "lookups_per_ray": dg["lookups"] / rays,
+            "samples_per_ray": samples / rays if samples else None,
+            "model_ms": model_ms, "measured_kernel_ms": statistics.median(kern_ms),
+            "round_trips_per_step": statistics.median(kern_ms) / model_ms if model_ms else None,
+            "note": "model = (lane march steps / 32) warp-steps x one L2 round trip (248 cycles) "
+                    "spread over every resident warp (SMs x 32), i.e. the frame time if every "
+                    "step were a single perfectly overlapped dependent L2 access; "
+                    "round_trips_per_step = measured / model"}
+
     # ---- e2e through the drop-in API (host frame out) ----
     e2e = None
-    host = None
-    volume = None
-    if world == 1 and (not args.no_e2e or args.orbit or not args.no_cpu):
+    host = volume.data if volume is not None else None
+    if world == 1 and volume is None and (not args.no_e2e or args.orbit or not args.no_cpu):
         host = dvol.read()  # the host Volume of the e2e / CPU legs (compact copy)
         volume = _attach(vx.Volume(dims=spec.dims, data=host), dvol)
+    if volume is not None:
         volume.content_hash()
     if not args.no_e2e:
         if world == 1:
@@ -620,7 +719,7 @@ def run_ours(args):
     if rank == 0:
         compact = torch.empty(nvox, dtype=torch.uint8, device="cuda")
         if host is not None:
-            compact.copy_(torch.from_numpy(host.reshape(-1)))
+            compact.copy_(torch.from_numpy(np.ascontiguousarray(host).reshape(-1)))
         else:
             table, n_shapes, seed, spots, k = _phantom_args(spec)
             _lib.call("vx_phantom_device", C.c_void_p(compact.data_ptr()), *spec.dims,
@@ -709,15 +808,19 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (device-generated phantom)",
-            "config": {"workload": workload_name(args.size, args.image, args.filter),
+            "config": {"workload": workload_name(args.size, args.image, args.filter, args.u16),
                        "volume": [args.size] * 3, "image": [W, H], "filter": args.filter,
                        "otsu_T": hist.otsu_threshold, "parallelism": par,
                        "l2": "flushed (256 MiB write) between steps, outside the step events",
-                       "skip": not args.no_skip, "phantom_gen_s": round(gen_s, 2)},
+                       "skip": not args.no_skip, "phantom_gen_s": round(gen_s, 2),
+                       "input": ("uint16 CT file via load_raw" if args.u16
+                                 else "uint8 phantom generated in HBM"),
+                       "ingest": ingest},
             "e2e": e2e,
             "e2e_orbit": orbit,
             "gpu_launches": launches,
             "roofline": roofline,
+            "latency_model": lat_model,
             "otsu_hist": hist_line,
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
