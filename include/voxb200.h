@@ -322,7 +322,10 @@ int vx_last_render_ms(float* ms_out);
 /* exact-skip structures for threshold thr, copied to host (tests):
  * level 0 = Chebyshev distance in 8^3 bricks to the nearest brick whose max
  * reaches thr (dims ceil(n/8)+2 per axis, 1-brick apron, capped at 24);
- * level 1 = the same over 4^3 cells (dims ceil(n/4)+2, capped at 32). */
+ * level 1 = the same over 4^3 cells (dims ceil(n/4)+2, capped at 32);
+ * level 8 + o = the orthant-o cell map: distance to the nearest cell >= thr
+ * among the cells a ray moving toward -axis a for every bit a of o (else
+ * +axis a) can still reach (the skip map of such rays). */
 int vx_volume_distance_map(vx_volume* vol, int32_t thr, int32_t level, uint8_t* host_out,
                            int64_t dims_out[3]);
 

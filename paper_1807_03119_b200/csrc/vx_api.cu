@@ -127,7 +127,11 @@ VolView vx_view(const vx_volume* v, const uint8_t* dist_map) {
   V.csy = v->csy;
   V.csz = v->csz;
   V.dist2 = dist_map ? dist_map + v->map_bytes + v->csz + v->csy + 1 : nullptr;
+  V.doct = nullptr;
+  V.oct_stride = 0;
+  V.oct_mask = 0;
 #ifdef VX_DEBUG_CHECKS
+  V.dolo = V.dohi = nullptr;
   V.lo = v->alloc;
   V.hi = v->alloc + v->alloc_bytes;
   V.d2lo = dist_map ? dist_map + v->map_bytes : nullptr;
@@ -385,6 +389,10 @@ extern "C" int vx_volume_destroy(vx_volume* v) {
   auto drop = [](MapSlot& m) {
     if (m.ready) cudaEventDestroy(m.ready);
     for (auto& u : m.uses) cudaEventDestroy(u.ev);
+    for (auto& e : m.oct_ready)
+      if (e) cudaEventDestroy(e);
+    if (m.oct) cudaFree(m.oct);
+    if (m.occ) cudaFree(m.occ);
   };
   for (auto& d : v->dist) drop(d);
   for (auto& a : v->acc) drop(a);
@@ -436,6 +444,7 @@ extern "C" int vx_volume_read(const vx_volume* v, uint8_t* host_out) {
 
 int vx_map_claim(vx_volume* v, MapSlot* m, cudaStream_t s) {
   for (auto& u : m->uses) VX_CUDA(cudaStreamWaitEvent(s, u.ev, 0));
+  m->oct_built = 0;  // the orthant maps belong to the old map
   VX_CUDA(cudaStreamWaitEvent(s, v->scratch_done, 0));
   return VX_OK;
 }
@@ -471,6 +480,32 @@ int vx_map_release(vx_volume* v, MapSlot* m, cudaStream_t s) {
   return VX_OK;
 }
 
+int vx_map_octants(vx_volume* v, MapSlot* m, unsigned need, unsigned* built_out, cudaStream_t s) {
+  need &= 0xffu;
+  if (need && !m->oct) {
+    // one block for all eight orthants, kept with the slot (reused by the
+    // next setting that takes it)
+    VX_CUDA(cudaMalloc(&m->oct, 8 * v->cmap_bytes));
+  }
+  for (int o = 0; o < 8; ++o) {
+    if (!((need >> o) & 1u)) continue;
+    if (!m->oct_ready[o]) VX_CUDA(cudaEventCreateWithFlags(&m->oct_ready[o], cudaEventDisableTiming));
+    if ((m->oct_built >> o) & 1u) {  // built by some stream: wait for it
+      VX_CUDA(cudaStreamWaitEvent(s, m->oct_ready[o], 0));
+      continue;
+    }
+    VX_CUDA(cudaStreamWaitEvent(s, v->scratch_done, 0));
+    int rc = vx_launch_dist_cells_oct(v, m->occ_src, m->oct + (uint64_t)o * v->cmap_bytes,
+                                      m->occ_thr, o, s);
+    if (rc) return rc;
+    VX_CUDA(cudaEventRecord(m->oct_ready[o], s));
+    VX_CUDA(cudaEventRecord(v->scratch_done, s));
+    m->oct_built |= 1u << o;
+  }
+  *built_out = m->oct_built & need;
+  return VX_OK;
+}
+
 int vx_get_dist_map(vx_volume* v, int thr, const uint8_t** map_out, MapSlot** slot_out,
                     cudaStream_t s) {
   *map_out = nullptr;
@@ -502,6 +537,8 @@ int vx_get_dist_map(vx_volume* v, int thr, const uint8_t** map_out, MapSlot** sl
   if (rc) return rc;
   rc = vx_launch_dist_map(v, thr, victim->map, s);
   if (rc) return rc;
+  victim->occ_src = v->cmax;  // orthant maps threshold the cell max map
+  victim->occ_thr = thr;
   if ((rc = vx_map_publish(v, victim, s))) return rc;
   if ((rc = vx_map_pin(victim, s))) return rc;
   victim->thr = thr;
@@ -513,14 +550,16 @@ int vx_get_dist_map(vx_volume* v, int thr, const uint8_t** map_out, MapSlot** sl
 
 extern "C" int vx_volume_distance_map(vx_volume* v, int32_t thr, int32_t level,
                                       uint8_t* host_out, int64_t dims_out[3]) {
-  if (!v || (level != 0 && level != 1)) {
+  const bool orthant = level >= 8 && level < 16;
+  if (!v || (level != 0 && level != 1 && !orthant)) {
     vx_set_error("vx_volume_distance_map: bad argument");
     return VX_EINVAL;
   }
+  const bool cells = level != 0;
   if (dims_out) {
-    dims_out[0] = level ? v->ncx + 2 : v->nbx + 2;
-    dims_out[1] = level ? v->ncy + 2 : v->nby + 2;
-    dims_out[2] = level ? v->ncz + 2 : v->nbz + 2;
+    dims_out[0] = cells ? v->ncx + 2 : v->nbx + 2;
+    dims_out[1] = cells ? v->ncy + 2 : v->nby + 2;
+    dims_out[2] = cells ? v->ncz + 2 : v->nbz + 2;
   }
   if (!host_out) return VX_OK;
   cudaStream_t s = vx_stream();
@@ -532,8 +571,21 @@ extern "C" int vx_volume_distance_map(vx_volume* v, int32_t thr, int32_t level,
     vx_set_error("vx_volume_distance_map: every map slot is in use");
     return VX_EINVAL;
   }
-  cudaError_t e = cudaMemcpyAsync(host_out, level ? map + v->map_bytes : map,
-                                  level ? v->cmap_bytes : v->map_bytes, cudaMemcpyDeviceToHost, s);
+  const uint8_t* src = level == 0 ? map : map + v->map_bytes;
+  if (orthant) {
+    unsigned built = 0;
+    {
+      std::lock_guard<std::mutex> lock(v->mu);
+      rc = vx_map_octants(v, slot, 1u << (level - 8), &built, s);
+    }
+    if (rc) {
+      vx_map_release(v, slot, s);
+      return rc;
+    }
+    src = slot->oct + (uint64_t)(level - 8) * v->cmap_bytes;
+  }
+  cudaError_t e = cudaMemcpyAsync(host_out, src, cells ? v->cmap_bytes : v->map_bytes,
+                                  cudaMemcpyDeviceToHost, s);
   rc = vx_map_release(v, slot, s);
   if (e != cudaSuccess) return vx_cuda_fail(e, "cudaMemcpyAsync(map)", __FILE__, __LINE__);
   if (rc) return rc;

@@ -57,9 +57,14 @@ struct VolView {
   int64_t bsy, bsz;       // strides of the brick maps
   const uint8_t* dist2;   // Chebyshev cell-distance map at cell (0,0,0)
   int64_t csy, csz;       // strides of the cell maps
+  // orthant maps (nullable): map of orthant o at doct + o * oct_stride (cell
+  // (0,0,0)); bit o of oct_mask set when that orthant's map is built
+  const uint8_t* doct;
+  int64_t oct_stride;
+  int oct_mask;
 #ifdef VX_DEBUG_CHECKS
-  // bounds of the padded allocation and of the cell map (checked build only)
-  const uint8_t *lo, *hi, *d2lo, *d2hi;
+  // bounds of the padded allocation and of the cell maps (checked build only)
+  const uint8_t *lo, *hi, *d2lo, *d2hi, *dolo, *dohi;
 #endif
 };
 
@@ -100,6 +105,16 @@ struct MapSlot {
   int pins = 0;
   cudaEvent_t ready = nullptr;
   std::vector<MapUse> uses;
+  // Orthant maps: per ray-direction orthant, the distance to
+  // the nearest occupied cell a ray of that orthant can still reach; built
+  // on demand from the slot's occupancy (occ_src >= occ_thr) for the
+  // orthants a frame's rays use.  oct: 8 * cmap_bytes, allocated on first use.
+  const uint8_t* occ_src = nullptr;
+  int occ_thr = 0;
+  uint8_t* occ = nullptr;  // accepted-cell occupancy kept for orthant builds (cmap_bytes)
+  uint8_t* oct = nullptr;
+  unsigned oct_built = 0;
+  cudaEvent_t oct_ready[8] = {};
 };
 
 struct DistEntry : MapSlot {
@@ -165,6 +180,11 @@ int vx_map_publish(vx_volume* v, MapSlot* m, cudaStream_t s);
 int vx_map_pin(MapSlot* m, cudaStream_t s);
 // unpin after the readers on s are enqueued (nullptr: no-op)
 int vx_map_release(vx_volume* v, MapSlot* m, cudaStream_t s);
+// caller holds v->mu and a pin of m: the orthant maps in `need` (bitmask) are
+// built (stream-ordered on s) or awaited; returns the built mask
+int vx_map_octants(vx_volume* v, MapSlot* m, unsigned need, unsigned* built_out, cudaStream_t s);
+int vx_launch_dist_cells_oct(const vx_volume* v, const uint8_t* occ, uint8_t* out, int thr, int oct,
+                             cudaStream_t s);
 
 // launchers implemented across translation units
 int vx_launch_hist(const uint8_t* dev, uint64_t n, uint64_t* dev_counts, cudaStream_t s);

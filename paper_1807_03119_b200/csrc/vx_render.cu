@@ -508,7 +508,16 @@ struct RayState {
   float bo[3];   // exit-face offset minus origin: (inv > 0 ? -1/8 : 4 + 1/8) - o
   float base;
   float tend;
+  const uint8_t* dmap;  // cell distance map the skips read (orthant or two-sided)
 };
+
+// the skip map of this ray: the map of its direction orthant when the frame
+// built it (bit a of the orthant = moving toward -axis a, the same test as
+// the exit-face choice in R.bo), else the two-sided Chebyshev map
+__device__ __forceinline__ void ray_skip_map(RayState& R, const VolView& V) {
+  const int oct = (R.inv[0] > 0.0f ? 0 : 1) | (R.inv[1] > 0.0f ? 0 : 2) | (R.inv[2] > 0.0f ? 0 : 4);
+  R.dmap = ((V.oct_mask >> oct) & 1) ? V.doct + oct * V.oct_stride : V.dist2;
+}
 
 __device__ __forceinline__ void ray_skip_consts(RayState& R) {
 #pragma unroll
@@ -680,10 +689,14 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
           const int cx = vx >> VX_CELL_SHIFT, cy = vy >> VX_CELL_SHIFT, cz = vz >> VX_CELL_SHIFT;
           // in-span samples truncate into [0, n]: inside the map's 1-cell apron
           VX_DIAG(dLookup);
-          VX_DCHECK(V.dist2 + (cz * (int)V.csz + cy * (int)V.csy + cx) >= V.d2lo &&
-                        V.dist2 + (cz * (int)V.csz + cy * (int)V.csy + cx) < V.d2hi,
+          VX_DCHECK((R.dmap == V.dist2 &&
+                     R.dmap + (cz * (int)V.csz + cy * (int)V.csy + cx) >= V.d2lo &&
+                     R.dmap + (cz * (int)V.csz + cy * (int)V.csy + cx) < V.d2hi) ||
+                        (R.dmap != V.dist2 &&
+                         R.dmap + (cz * (int)V.csz + cy * (int)V.csy + cx) >= V.dolo &&
+                         R.dmap + (cz * (int)V.csz + cy * (int)V.csy + cx) < V.dohi),
                     "cell (%d, %d, %d) outside the distance map", cx, cy, cz);
-          const int D = __ldg(V.dist2 + (cz * (int)V.csz + cy * (int)V.csy + cx));
+          const int D = __ldg(R.dmap + (cz * (int)V.csz + cy * (int)V.csy + cx));
           float lim = -1.0f;
           if (D >= M.skip_min_d) {
             // cells within Chebyshev distance D-1 of this one: the box
@@ -1223,6 +1236,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
         R.d[c] = __double2float_rn(d[c]);
       }
       ray_skip_consts(R);
+      ray_skip_map(R, a.V);
       R.base = __double2float_rn(te);
       R.tend = __double2float_rn(tx_);
       // Per-ray budget = this ray's own max(1, ceil(span/step) + 1) <= the
@@ -1506,6 +1520,7 @@ __global__ void march_rays_kernel(VolView V, MarchD M, FiltD F, const double* __
         R.d[c] = __double2float_rn(dirs[3 * r + c]);
       }
       ray_skip_consts(R);
+      ray_skip_map(R, V);
       R.base = __double2float_rn(te);
       R.tend = __double2float_rn(tx);
       limit = max_steps[r];
@@ -1889,6 +1904,48 @@ static double trace_us() {
     }                                                                             \
   } while (0)
 
+// Orthant skip maps: VOXB200_ORTHANT=0 renders on the
+// two-sided Chebyshev maps only
+static bool orthant_maps_on() {
+  static const bool on = [] {
+    const char* e = getenv("VOXB200_ORTHANT");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
+// The direction orthants of a frame's primary rays.  d = (fwd + u right) +
+// v up before normalisation (which keeps signs) is affine in the pixel's
+// (u, v), so per axis its range over the image is spanned by the four
+// corner pixels; an axis whose range reaches within 1e-9 of zero may be
+// either sign.  A ray whose orthant is not in the set falls back to the
+// two-sided map on the device, so this only decides what gets built.
+static unsigned frame_octants(const vx_ray_setup* rs) {
+  const double W = rs->width, H = rs->height;
+  const double us[2] = {((2.0 * 0.5) / W - 1.0) * rs->tan_f * rs->aspect,
+                        ((2.0 * (W - 0.5)) / W - 1.0) * rs->tan_f * rs->aspect};
+  const double vs[2] = {(1.0 - (2.0 * 0.5) / H) * rs->tan_f, (1.0 - (2.0 * (H - 0.5)) / H) * rs->tan_f};
+  unsigned can_pos = 0, can_neg = 0;
+  for (int a = 0; a < 3; ++a) {
+    double lo = 1e300, hi = -1e300;
+    for (double u : us)
+      for (double v : vs) {
+        const double d = (rs->fwd[a] + u * rs->right[a]) + v * rs->up[a];
+        lo = d < lo ? d : lo;
+        hi = d > hi ? d : hi;
+      }
+    if (hi > -1e-9) can_pos |= 1u << a;
+    if (lo < 1e-9) can_neg |= 1u << a;
+  }
+  unsigned mask = 0;
+  for (int o = 0; o < 8; ++o) {
+    bool ok = true;
+    for (int a = 0; a < 3; ++a) ok = ok && (((o >> a) & 1) ? (can_neg >> a) & 1 : (can_pos >> a) & 1);
+    if (ok) mask |= 1u << o;
+  }
+  return mask;
+}
+
 // Accepted-cell distance map for the render's filter setting (nullptr: use
 // the raw candidate map).  Policy: a setting seen for the first time renders
 // on the raw map (one-shot frames such as a filter comparison pay nothing);
@@ -1959,7 +2016,9 @@ static int get_accept_map(vx_volume* v, const RenderArgs& a, bool checked, const
   e->valid = false;  // until built
   int rc = vx_map_claim(v, e, s);
   if (rc) return rc;
-  uint8_t* occ = v->scratch;  // the volume's build scratch (claimed above)
+  // the occupancy stays with the slot: the orthant maps are built from it
+  if (!e->occ) VX_CUDA(cudaMalloc(&e->occ, v->cmap_bytes));
+  uint8_t* occ = e->occ;
   VX_CUDA(cudaMemsetAsync(occ, 0, v->cmap_bytes, s));
   VX_CUDA(cudaMemsetAsync(e->map, 0, v->map_bytes, s));  // coarse level unused: no skip
   VX_TRACE("  acc scratch", tt);
@@ -1984,6 +2043,8 @@ static int get_accept_map(vx_volume* v, const RenderArgs& a, bool checked, const
   VX_CHECK_LAUNCH();
   rc = vx_launch_dist_cells(v, occ, e->map + v->map_bytes, 1, s);
   if (rc) return rc;
+  e->occ_src = occ;
+  e->occ_thr = 1;
   VX_TRACE("  acc launches", tt);
   // other streams wait on the slot's ready event (no host sync under mu)
   if ((rc = vx_map_publish(v, e, s))) return rc;
@@ -2209,6 +2270,25 @@ static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_p
     if (!dist) a.M.skip = 0;
   }
   a.V = vx_view(vol, dist);
+  if (dist && pin.m && orthant_maps_on()) {
+    // the orthant maps of the directions this frame's rays take
+    unsigned built = 0;
+    {
+      std::lock_guard<std::mutex> lock(vol->mu);
+      rc = vx_map_octants(vol, pin.m, frame_octants(rs), &built, s);
+    }
+    if (rc) return rc;
+    VX_TRACE("orthant_maps", tt);
+    if (built) {
+      a.V.doct = pin.m->oct + vol->csz + vol->csy + 1;
+      a.V.oct_stride = (int64_t)vol->cmap_bytes;
+      a.V.oct_mask = (int)built;
+#ifdef VX_DEBUG_CHECKS
+      a.V.dolo = pin.m->oct;
+      a.V.dohi = pin.m->oct + 8 * vol->cmap_bytes;
+#endif
+    }
+  }
   a.O.pixels = o->pixels;
   a.O.hit_voxel = o->hit_voxel;
   a.O.hit_t = o->hit_t;

@@ -55,9 +55,12 @@ constexpr int kRowsPerBlock = 64;
 // 256 threads: the 8 warps stage / store the 64 rows (one row per warp at a
 // time, lanes along x: coalesced, no per-byte index division), the first 64
 // threads sweep one row each
+template <int DIR>
 __global__ void __launch_bounds__(256) dist_first_x_kernel(
     const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int mx, int64_t rows, int thr,
     int cap) {
+  // DIR 0: two-sided (Chebyshev); +1: distance to the nearest occupied cell
+  // at x' >= x (rays moving toward +x); -1: at x' <= x (orthant maps)
   extern __shared__ uint8_t rowbuf[];
   const int pitch = mx | 1;  // odd pitch: threads sweeping rows hit distinct banks
   const int64_t r0 = (int64_t)blockIdx.x * kRowsPerBlock;
@@ -69,15 +72,25 @@ __global__ void __launch_bounds__(256) dist_first_x_kernel(
   __syncthreads();
   if ((int)threadIdx.x < nr) {
     uint8_t* L = rowbuf + threadIdx.x * pitch;
-    int last = -(1 << 20);
-    for (int x = 0; x < mx; ++x) {  // forward: distance to the last occupied cell
-      if (L[x] >= thr) last = x;
-      L[x] = (uint8_t)min(cap, x - last);
+    if (DIR <= 0) {
+      int last = -(1 << 20);
+      for (int x = 0; x < mx; ++x) {  // forward: distance to the last occupied cell
+        if (L[x] >= thr) last = x;
+        L[x] = (uint8_t)min(cap, x - last);
+      }
     }
-    int next = 1 << 20;
-    for (int x = mx - 1; x >= 0; --x) {  // backward, and the minimum of both
-      if (L[x] == 0) next = x;
-      L[x] = (uint8_t)min((int)L[x], min(cap, next - x));
+    if (DIR == 0) {
+      int next = 1 << 20;
+      for (int x = mx - 1; x >= 0; --x) {  // backward, and the minimum of both
+        if (L[x] == 0) next = x;
+        L[x] = (uint8_t)min((int)L[x], min(cap, next - x));
+      }
+    } else if (DIR > 0) {
+      int next = 1 << 20;
+      for (int x = mx - 1; x >= 0; --x) {  // distance to the next occupied cell
+        if (L[x] >= thr) next = x;
+        L[x] = (uint8_t)min(cap, next - x);
+      }
     }
   }
   __syncthreads();
@@ -100,10 +113,11 @@ __global__ void __launch_bounds__(256) dist_first_x_kernel(
 // them then sweep one line each.
 constexpr int kSweepCols = 64;
 
-template <int AXIS>
+template <int AXIS, int DIR>
 __global__ void __launch_bounds__(4 * kSweepCols) dist_sweep_kernel(const uint8_t* __restrict__ src,
                                                                    uint8_t* __restrict__ dst,
                                                                    int mx, int my, int mz, int cap) {
+  // DIR 0: D = min(L, R); DIR +1: R only (cells at l' >= l); DIR -1: L only
   extern __shared__ uint8_t sweep_sm[];
   const int n = AXIS == 1 ? my : mz;
   uint8_t* val = sweep_sm;                                   // [n][64] v, then D
@@ -122,31 +136,37 @@ __global__ void __launch_bounds__(4 * kSweepCols) dist_sweep_kernel(const uint8_
   const int tx = threadIdx.x;
   if (tx < kSweepCols && x0 + tx < mx) {
     constexpr uint16_t kNone = 0xffffu;
-    // left sweep
-    for (int w = 0; w < 32; ++w) last[w * kSweepCols + tx] = kNone;
-    int m = cap;
-    for (int l = 0; l < n; ++l) {
-      const int v = val[l * kSweepCols + tx];
-      if (v < cap) last[v * kSweepCols + tx] = (uint16_t)l;
-      if (m < cap) {
-        const int lm = last[m * kSweepCols + tx];
-        if (lm == kNone || l - lm > m) m = min(m + 1, cap);
+    if (DIR <= 0) {  // left sweep
+      for (int w = 0; w < 32; ++w) last[w * kSweepCols + tx] = kNone;
+      int m = cap;
+      for (int l = 0; l < n; ++l) {
+        const int v = val[l * kSweepCols + tx];
+        if (v < cap) last[v * kSweepCols + tx] = (uint16_t)l;
+        if (m < cap) {
+          const int lm = last[m * kSweepCols + tx];
+          if (lm == kNone || l - lm > m) m = min(m + 1, cap);
+        }
+        if (v < m) m = v;
+        left[l * kSweepCols + tx] = (uint8_t)m;
       }
-      if (v < m) m = v;
-      left[l * kSweepCols + tx] = (uint8_t)m;
     }
-    // right sweep, then D = min(L, R) in place of v (v(l) is not read again)
-    for (int w = 0; w < 32; ++w) last[w * kSweepCols + tx] = kNone;
-    m = cap;
-    for (int l = n - 1; l >= 0; --l) {
-      const int v = val[l * kSweepCols + tx];
-      if (v < cap) last[v * kSweepCols + tx] = (uint16_t)l;
-      if (m < cap) {
-        const int lm = last[m * kSweepCols + tx];
-        if (lm == kNone || lm - l > m) m = min(m + 1, cap);
+    if (DIR < 0) {
+      for (int l = 0; l < n; ++l) val[l * kSweepCols + tx] = left[l * kSweepCols + tx];
+    } else {
+      // right sweep, then D = min(L, R) (or R alone) in place of v (v(l) is
+      // not read again)
+      for (int w = 0; w < 32; ++w) last[w * kSweepCols + tx] = kNone;
+      int m = cap;
+      for (int l = n - 1; l >= 0; --l) {
+        const int v = val[l * kSweepCols + tx];
+        if (v < cap) last[v * kSweepCols + tx] = (uint16_t)l;
+        if (m < cap) {
+          const int lm = last[m * kSweepCols + tx];
+          if (lm == kNone || lm - l > m) m = min(m + 1, cap);
+        }
+        if (v < m) m = v;
+        val[l * kSweepCols + tx] = (uint8_t)(DIR == 0 ? min(m, (int)left[l * kSweepCols + tx]) : m);
       }
-      if (v < m) m = v;
-      val[l * kSweepCols + tx] = (uint8_t)min(m, (int)left[l * kSweepCols + tx]);
     }
   }
   __syncthreads();
@@ -302,13 +322,14 @@ int vx_launch_brick_max(vx_volume* v, cudaStream_t s) {
 
 // tmp: an intermediate of mx*my*mz bytes (the volume's build scratch: a
 // stream-ordered allocation here grew the pool inside a frame, 1-20 ms)
-static int dist_transform(const uint8_t* maxmap, uint8_t* out, int mx, int my, int mz, int thr,
-                          int cap, uint8_t* tmp, cudaStream_t s) {
+template <int DX, int DY, int DZ>
+static int dist_transform_dir(const uint8_t* maxmap, uint8_t* out, int mx, int my, int mz, int thr,
+                              int cap, uint8_t* tmp, cudaStream_t s) {
   const int64_t rows = (int64_t)my * mz;
   const size_t s0 = (size_t)kRowsPerBlock * (mx | 1);
-  int rc = smem_opt_in((const void*)dist_first_x_kernel, s0);
+  int rc = smem_opt_in((const void*)dist_first_x_kernel<DX>, s0);
   if (rc) return rc;
-  dist_first_x_kernel<<<(unsigned)((rows + kRowsPerBlock - 1) / kRowsPerBlock), 256, s0, s>>>(
+  dist_first_x_kernel<DX><<<(unsigned)((rows + kRowsPerBlock - 1) / kRowsPerBlock), 256, s0, s>>>(
       maxmap, out, mx, rows, thr, cap);
   VX_CHECK_LAUNCH();
   const unsigned gx = (unsigned)((mx + kSweepCols - 1) / kSweepCols);
@@ -319,15 +340,20 @@ static int dist_transform(const uint8_t* maxmap, uint8_t* out, int mx, int my, i
   }
   auto sweep_smem = [](int n) { return (size_t)2 * n * kSweepCols + 64 * kSweepCols; };
   const size_t s1 = sweep_smem(my), s2 = sweep_smem(mz);
-  if ((rc = smem_opt_in((const void*)dist_sweep_kernel<1>, s1))) return rc;
-  dist_sweep_kernel<1><<<dim3(gx, (unsigned)mz), 4 * kSweepCols, s1, s>>>(out, tmp, mx, my, mz,
-                                                                             cap);
+  if ((rc = smem_opt_in((const void*)dist_sweep_kernel<1, DY>, s1))) return rc;
+  dist_sweep_kernel<1, DY><<<dim3(gx, (unsigned)mz), 4 * kSweepCols, s1, s>>>(out, tmp, mx, my,
+                                                                               mz, cap);
   VX_CHECK_LAUNCH();
-  if ((rc = smem_opt_in((const void*)dist_sweep_kernel<2>, s2))) return rc;
-  dist_sweep_kernel<2><<<dim3(gx, (unsigned)my), 4 * kSweepCols, s2, s>>>(tmp, out, mx, my, mz,
-                                                                             cap);
+  if ((rc = smem_opt_in((const void*)dist_sweep_kernel<2, DZ>, s2))) return rc;
+  dist_sweep_kernel<2, DZ><<<dim3(gx, (unsigned)my), 4 * kSweepCols, s2, s>>>(tmp, out, mx, my,
+                                                                               mz, cap);
   VX_CHECK_LAUNCH();
   return VX_OK;
+}
+
+static int dist_transform(const uint8_t* maxmap, uint8_t* out, int mx, int my, int mz, int thr,
+                          int cap, uint8_t* tmp, cudaStream_t s) {
+  return dist_transform_dir<0, 0, 0>(maxmap, out, mx, my, mz, thr, cap, tmp, s);
 }
 
 // coarse (bricks) then fine (cells) Chebyshev distance maps of thr into `map`
@@ -343,6 +369,32 @@ int vx_launch_dist_cells(const vx_volume* v, const uint8_t* occ, uint8_t* out, i
                          cudaStream_t s) {
   return dist_transform(occ, out, v->ncx + 2, v->ncy + 2, v->ncz + 2, thr, VX_FINE_CAP,
                         v->scratch + v->cmap_bytes, s);
+}
+
+// Orthant map `oct` (bit a set: rays move toward -axis a): the Chebyshev
+// distance to the nearest occupied cell among those a ray of that orthant
+// can still reach, D(c) = min over occupied o with s_a (o_a - c_a) >= 0 of
+// max_a s_a (o_a - c_a) -- separable like the two-sided map, with one-sided
+// sweeps (SURVEY Appendix A skip argument, DESIGN.md §5 "orthant maps").
+int vx_launch_dist_cells_oct(const vx_volume* v, const uint8_t* occ, uint8_t* out, int thr, int oct,
+                             cudaStream_t s) {
+  const int mx = v->ncx + 2, my = v->ncy + 2, mz = v->ncz + 2;
+  uint8_t* tmp = v->scratch + v->cmap_bytes;
+#define VX_OCT(o, dx, dy, dz) \
+  case o: return dist_transform_dir<dx, dy, dz>(occ, out, mx, my, mz, thr, VX_FINE_CAP, tmp, s)
+  switch (oct) {
+    VX_OCT(0, 1, 1, 1);
+    VX_OCT(1, -1, 1, 1);
+    VX_OCT(2, 1, -1, 1);
+    VX_OCT(3, -1, -1, 1);
+    VX_OCT(4, 1, 1, -1);
+    VX_OCT(5, -1, 1, -1);
+    VX_OCT(6, 1, -1, -1);
+    VX_OCT(7, -1, -1, -1);
+    default:
+      return dist_transform(occ, out, mx, my, mz, thr, VX_FINE_CAP, tmp, s);
+  }
+#undef VX_OCT
 }
 
 int vx_launch_cell_max(vx_volume* v, cudaStream_t s) {

@@ -211,3 +211,45 @@ def test_distance_map_is_exact_chebyshev(vx):
     occ2 = np.zeros((ncz + 2, ncy + 2, ncx + 2), dtype=bool)
     occ2[1:-1, 1:-1, 1:-1] = cmax >= 100
     assert np.array_equal(fm, _brute_distance(occ2, 32))
+
+
+def _brute_orthant(occ: np.ndarray, cap: int, oct: int) -> np.ndarray:
+    """min over occupied o with s_a (o_a - c_a) >= 0 (s_a = -1 if bit a of
+    oct, axes x, y, z) of max_a s_a (o_a - c_a), capped."""
+    sx, sy, sz = (-1 if (oct >> a) & 1 else 1 for a in range(3))
+    mz, my, mx = occ.shape
+    zz, yy, xx = np.meshgrid(np.arange(mz), np.arange(my), np.arange(mx), indexing="ij")
+    out = np.full(occ.shape, cap, dtype=np.int64)
+    for oz, oy, ox in np.argwhere(occ):
+        dx, dy, dz = sx * (ox - xx), sy * (oy - yy), sz * (oz - zz)
+        ok = (dx >= 0) & (dy >= 0) & (dz >= 0)
+        d = np.where(ok, np.maximum(np.maximum(dx, dy), dz), cap)
+        out = np.minimum(out, d)
+    return np.minimum(out, cap)
+
+
+def test_orthant_maps_exact(vx):
+    """The eight orthant skip maps equal a brute-force one-sided Chebyshev
+    distance over the 4^3 cells (including lines longer than the cap)."""
+    from paper_1807_03119_b200.volume import device_volume
+
+    rs = np.random.default_rng(7)
+    data = rs.integers(0, 50, (150, 37, 29), dtype=np.uint8)
+    for _ in range(9):
+        z, y, x = rs.integers(0, 150), rs.integers(0, 37), rs.integers(0, 29)
+        data[z, y, x] = 220
+    v = vx.Volume(dims=(29, 37, 150), data=data)
+    dv = device_volume(v)
+    c = 4
+    ncz, ncy, ncx = (150 + c - 1) // c, (37 + c - 1) // c, (29 + c - 1) // c
+    pad = np.zeros((ncz * c, ncy * c, ncx * c), dtype=np.uint8)
+    pad[:150, :37, :29] = data
+    cmax = pad.reshape(ncz, c, ncy, c, ncx, c).max(axis=(1, 3, 5))
+    occ = np.zeros((ncz + 2, ncy + 2, ncx + 2), dtype=bool)
+    occ[1:-1, 1:-1, 1:-1] = cmax >= 100
+    iso = dv.distance_map(100, level=1).astype(np.int64)
+    for o in range(8):
+        got = dv.distance_map(100, level=8 + o).astype(np.int64)
+        want = _brute_orthant(occ, 32, o)
+        assert np.array_equal(got, want), o
+        assert np.all(got >= iso)  # one-sided: never shorter than the two-sided map
