@@ -127,6 +127,11 @@ VolView vx_view(const vx_volume* v, const uint8_t* dist_map) {
   V.csy = v->csy;
   V.csz = v->csz;
   V.dist2 = dist_map ? dist_map + v->map_bytes + v->csz + v->csy + 1 : nullptr;
+#if VX_BRICK_LAYOUT
+  V.bricks = v->bricks;
+  V.bbx = v->bbx;
+  V.bby = v->bby;
+#endif
   V.doct = nullptr;
   V.oct_stride = 0;
   V.oct_mask = 0;
@@ -223,6 +228,15 @@ int vx_volume_finish(vx_volume* v, const uint8_t* compact_dev, cudaStream_t s) {
   p.kind = cudaMemcpyDeviceToDevice;
   VX_CUDA(cudaMemcpy3DAsync(&p, s));
   VX_CUDA(cudaMemsetAsync(v->bmax, 0, v->map_bytes + v->cmap_bytes, s));
+#if VX_BRICK_LAYOUT
+  v->bbx = (int)((v->nx + 2 * VX_PAD + 7) / 8);
+  v->bby = (int)((v->ny + 2 * VX_PAD + 7) / 8);
+  v->bbz = (int)((v->nz + 2 * VX_PAD + 7) / 8);
+  v->bricks_bytes = (uint64_t)v->bbx * v->bby * v->bbz * 512;
+  if (!v->bricks) VX_CUDA(cudaMalloc(&v->bricks, v->bricks_bytes));
+  rc = vx_launch_brickify(v, s);
+  if (rc) return rc;
+#endif
   rc = vx_launch_brick_max(v, s);
   if (rc) return rc;
   rc = vx_launch_cell_max(v, s);
@@ -399,6 +413,7 @@ extern "C" int vx_volume_destroy(vx_volume* v) {
   if (v->scratch_done) cudaEventDestroy(v->scratch_done);
   if (v->bmax) cudaFree(v->bmax);
   if (v->alloc) cudaFree(v->alloc);
+  if (v->bricks) cudaFree(v->bricks);
   if (cur != v->device) cudaSetDevice(cur);
   delete v;
   return VX_OK;

@@ -10,6 +10,15 @@
 
 #include "../../include/voxb200.h"
 
+// Voxel layout of the replica K4 reads (A/B): 0 = linear
+// (x fastest, 16-voxel zero apron), 1 = 8^3 bricks of 512 B (linear inside:
+// a 32 B sector is 8x4x1 voxels), 2 = 8^3 bricks, Morton order inside (a
+// sector is 4x4x2 voxels).  Bricked builds keep the linear replica for the
+// other kernels and add a bricked copy for K4.
+#ifndef VX_BRICK_LAYOUT
+#define VX_BRICK_LAYOUT 0
+#endif
+
 // Zero apron around the volume (voxels).  Covers the march's +/-1 voxel
 // truncation slop, Sobel (reach 1) and every filter with reach <= VX_PAD-1;
 // larger reach switches the filter to bounds-checked reads (same border
@@ -26,6 +35,16 @@
 #define VX_CELL_SHIFT 2
 #define VX_FINE_CAP 32
 #define VX_DIST_CACHE 4
+
+// offset of voxel (x, y, z) & 7 inside its 8^3 brick
+__host__ __device__ __forceinline__ int vx_in_brick(int x, int y, int z) {
+#if VX_BRICK_LAYOUT == 2
+  auto spread = [](int v) { return (v & 1) | ((v & 2) << 2) | ((v & 4) << 4); };
+  return spread(x) | (spread(y) << 1) | (spread(z) << 2);
+#else
+  return (z << 6) | (y << 3) | x;
+#endif
+}
 
 // ---------------------------------------------------------------------------
 // error plumbing
@@ -57,6 +76,10 @@ struct VolView {
   int64_t bsy, bsz;       // strides of the brick maps
   const uint8_t* dist2;   // Chebyshev cell-distance map at cell (0,0,0)
   int64_t csy, csz;       // strides of the cell maps
+#if VX_BRICK_LAYOUT
+  const uint8_t* bricks;  // bricked copy: brick (bx, by, bz) of the apron-padded grid
+  int bbx, bby;           // bricks per row / per plane row (apron included)
+#endif
   // orthant maps (nullable): map of orthant o at doct + o * oct_stride (cell
   // (0,0,0)); bit o of oct_mask set when that orthant's map is built
   const uint8_t* doct;
@@ -160,6 +183,9 @@ struct vx_volume {
   // streams are ordered through scratch_done
   uint8_t* scratch;
   cudaEvent_t scratch_done;
+  uint8_t* bricks;  // VX_BRICK_LAYOUT: the bricked copy K4 reads
+  int bbx, bby, bbz;
+  uint64_t bricks_bytes;
   uint64_t stamp;
   uint64_t counts[256];
   std::mutex mu;
@@ -198,6 +224,8 @@ int vx_launch_brick_max(vx_volume* v, cudaStream_t s);
 int vx_launch_dist_map(const vx_volume* v, int thr, uint8_t* map, cudaStream_t s);
 // (callers hold v->mu: the builds use v->scratch)
 int vx_launch_cell_max(vx_volume* v, cudaStream_t s);
+// VX_BRICK_LAYOUT: the bricked copy of the (finished) linear replica
+int vx_launch_brickify(vx_volume* v, cudaStream_t s);
 // Chebyshev cell-distance map (cap VX_FINE_CAP) of the cells whose value in
 // `occ` (cell-map layout, apron included) is >= thr
 int vx_launch_dist_cells(const vx_volume* v, const uint8_t* occ, uint8_t* out, int thr,

@@ -189,6 +189,13 @@ __device__ __forceinline__ int rd(const VolView& V, long long x, long long y, lo
   VX_DCHECK(V.origin + (z * V.sz + y * V.sy + x) >= V.lo &&
                 V.origin + (z * V.sz + y * V.sy + x) < V.hi,
             "voxel (%lld, %lld, %lld) outside the allocation", x, y, z);
+#if VX_BRICK_LAYOUT
+  {
+    const int X = (int)x + VX_PAD, Y = (int)y + VX_PAD, Z = (int)z + VX_PAD;
+    const int b = ((Z >> 3) * V.bby + (Y >> 3)) * V.bbx + (X >> 3);
+    return __ldg(V.bricks + ((size_t)b << 9) + vx_in_brick(X & 7, Y & 7, Z & 7));
+  }
+#endif
   return __ldg(V.origin + (z * V.sz + y * V.sy + x));
 }
 

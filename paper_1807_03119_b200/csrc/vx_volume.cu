@@ -295,7 +295,39 @@ __global__ void u16_dither_kernel(const uint8_t* __restrict__ v8, uint64_t n, ui
   }
 }
 
+// one thread per 8-voxel brick row (bz, by, bx, z, y): 8 bytes of the
+// linear apron layout (X = x + VX_PAD multiple of 8: 8-byte aligned) into
+// the brick; bytes beyond the padded grid are zero
+__global__ void brickify_kernel(const uint8_t* __restrict__ lin, int64_t sy, int64_t sz,
+                                int64_t px, int64_t py, int64_t pz, uint8_t* __restrict__ bricks,
+                                int bbx, int bby, int bbz) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nrows = (int64_t)bbx * bby * bbz * 64;
+  if (r >= nrows) return;
+  const int64_t b = r >> 6;
+  const int zy = (int)(r & 63), zi = zy >> 3, yi = zy & 7;
+  const int bx = (int)(b % bbx), by = (int)((b / bbx) % bby), bz = (int)(b / ((int64_t)bbx * bby));
+  const int64_t X = (int64_t)bx * 8, Y = (int64_t)by * 8 + yi, Z = (int64_t)bz * 8 + zi;
+  uint2 w = make_uint2(0u, 0u);
+  if (Y < py && Z < pz && X + 8 <= px)
+    w = __ldg(reinterpret_cast<const uint2*>(lin + Z * sz + Y * sy + X));
+  else if (Y < py && Z < pz)
+    for (int k = 0; k < 8 && X + k < px; ++k)
+      (k < 4 ? w.x : w.y) |= (uint32_t)lin[Z * sz + Y * sy + X + k] << (8 * (k & 3));
+  uint8_t* dst = bricks + (b << 9);
+  for (int k = 0; k < 8; ++k)
+    dst[vx_in_brick(k, yi, zi)] = (uint8_t)(((k < 4 ? w.x : w.y) >> (8 * (k & 3))) & 0xffu);
+}
+
 }  // namespace
+
+int vx_launch_brickify(vx_volume* v, cudaStream_t s) {
+  const int64_t nrows = (int64_t)v->bbx * v->bby * v->bbz * 64;
+  brickify_kernel<<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(
+      v->alloc, v->sy, v->sz, v->px, v->py, v->pz, v->bricks, v->bbx, v->bby, v->bbz);
+  VX_CHECK_LAUNCH();
+  return VX_OK;
+}
 
 extern "C" int vx_u16_dither_device(const uint8_t* dev_v8, uint64_t n, uint64_t i0, uint64_t seed,
                                     uint16_t* dev_out, void* stream) {
