@@ -90,6 +90,14 @@ constexpr bool kSplitRays = VX_SPLIT_RAYS && kWarpsPerBlock == 4;
 #ifndef VX_GROUP_PIPE
 #define VX_GROUP_PIPE 0
 #endif
+// needy lanes from which each loads its own sample group instead of the
+// warp's shuffle-fed passes, in skipping frames (33: never).  Measured
+// (profiles/r2/r2_ab_own_group.txt): 8/12/20 cost the skipping frames 6-9 %
+// (bench, C3 sigma/entropy) even when rarely taken, so skipping kernels keep
+// the passes; the no-skip kernel (SKIP = false) always loads its own groups.
+#ifndef VX_OWN_MIN
+#define VX_OWN_MIN 33
+#endif
 
 struct MarchD {
   float s;        // f32(step)
@@ -622,7 +630,7 @@ __device__ __forceinline__ int first_beyond(float base, const MarchD& M, float l
 // wl: this warp's 32-int shared scratch.  All 32 lanes must call.
 // limit = the lane's sample budget.  Returns kHit, kMiss (left the span or
 // inactive) or kExhausted (budget ran out while still inside the span).
-template <int KIND, bool CHECKED, bool DIAG, bool BUDGET>
+template <int KIND, bool CHECKED, bool DIAG, bool BUDGET, bool SKIP = true>
 __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const double* lut,
                      const RayState& R, bool active, int limit, int done0, int stop,
                      float& ht, int& hidx, unsigned& nsamp, Diag& dg, WarpScratch* ws) {
@@ -689,7 +697,7 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
           // later samples of this chunk are beyond the exit too and the
           // next chunk's base >= t_k: the reference drops the ray
           status = kMiss;
-        } else if (M.skip) {
+        } else if (SKIP && M.skip) {
           const int vx = __float2int_rz(pos1(R.o[0], tk, R.d[0]));
           const int vy = __float2int_rz(pos1(R.o[1], tk, R.d[1]));
           const int vz = __float2int_rz(pos1(R.o[2], tk, R.d[2]));
@@ -805,9 +813,35 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
     if (gm) {
       const int nr = __popc(gm);
       const int rank = __popc(gm & ((1u << lane) - 1u));
+      unsigned my_c = 0, my_v = 0;
+      if (nr >= (SKIP ? VX_OWN_MIN : 0)) {
+        // most lanes need samples (dense regions, no-skip frames): each loads
+        // its own kGroup samples, all in flight together -- ~3x fewer issue
+        // slots per sample than the shuffle-fed passes below, which pay off
+        // only when few lanes need samples.  Same samples, same arithmetic.
+        if (need) {
+          int raws[kGroup];
+#pragma unroll
+          for (int j = 0; j < kGroup; ++j) {
+            const int kk = min(k + j, max(m - 1, 0));
+            const float t = sample_t(base, M.s, kk);
+            float px = pos1(R.o[0], t, R.d[0]), py = pos1(R.o[1], t, R.d[1]),
+                  pz = pos1(R.o[2], t, R.d[2]);
+            if (M.need_clip) {
+              px = clip1(px, M.xmax);
+              py = clip1(py, M.ymax);
+              pz = clip1(pz, M.zmax);
+            }
+            raws[j] = rd<false>(V, __float2int_rz(px), __float2int_rz(py), __float2int_rz(pz));
+            if (k + j < m && t <= tend) my_v |= 1u << j;
+          }
+#pragma unroll
+          for (int j = 0; j < kGroup; ++j)
+            if (((my_v >> j) & 1u) && raws[j] >= M.thr) my_c |= 1u << j;
+        }
+      } else {
       if (need) wl[rank] = (int)lane;
       __syncwarp();
-      unsigned my_c = 0, my_v = 0;
       // one pass = 4 rays x 8 samples; two passes are issued back to back so
       // their loads are in flight together
       auto pass_load = [&](int b, int& raw, bool& inr) {
@@ -880,6 +914,7 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
       }
       }
       __syncwarp();
+      }  // cooperative passes
       // ---- cooperative filter evaluation: every candidate of every needy
       // lane is evaluated by some lane of the warp at once (filter values are
       // pure functions of the voxel), then each owner takes its FIRST passing
@@ -1143,7 +1178,7 @@ __device__ unsigned g_warp_sm[1 << 20];
 __device__ unsigned g_warp_diag[9 << 20];
 #endif
 
-template <int KIND, bool CHECKED, bool DIAG, bool BUDGET>
+template <int KIND, bool CHECKED, bool DIAG, bool BUDGET, bool SKIP = true>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kWarpsPerBlock)
     raycast_kernel(const RenderArgs a) {
   __shared__ double lut[KIND == VX_FILTER_ENTROPY ? 256 : 1];
@@ -1275,7 +1310,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
   }
   // all lanes of the warp march together (cooperative sample loads)
   {
-    int st = march<KIND, CHECKED, DIAG, BUDGET>(a.V, a.M, a.F, lut, R, live, limit, done0, stop,
+    int st = march<KIND, CHECKED, DIAG, BUDGET, SKIP>(a.V, a.M, a.F, lut, R, live, limit, done0, stop,
                                                 ht, hidx, nsamp, dg, &wsc[tid >> 5]);
     if (nseg > 1) {
       // merge pairwise toward segment 0: an earlier segment's hit wins
@@ -1715,6 +1750,8 @@ void launch_raycast(const RenderArgs& a, int grid, cudaStream_t s) {
     raycast_kernel<KIND, CHECKED, false, true><<<grid, blk, 0, s>>>(a);
   else if (a.O.diag)
     raycast_kernel<KIND, CHECKED, true, false><<<grid_u, blk, 0, s>>>(a);
+  else if (!a.M.skip)  // full traversal (skipping off, or thr == 0): lean own-group loads
+    raycast_kernel<KIND, CHECKED, false, false, false><<<grid_u, blk, 0, s>>>(a);
   else
     raycast_kernel<KIND, CHECKED, false, false><<<grid_u, blk, 0, s>>>(a);
 }
