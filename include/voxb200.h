@@ -260,6 +260,9 @@ int vx_group_create(int32_t rank, int32_t world, int64_t max_pixels, vx_group** 
                     uint8_t* blob_out);
 int vx_group_connect(vx_group* g, const uint8_t* blobs, int32_t sync);
 int vx_group_info(const vx_group* g, int32_t* sync_out, uint32_t* frame_out);
+/* VX_OK when this device supports the stream memory operations of
+ * VX_GROUP_SYNC_DEVICE (all ranks should agree before connecting). */
+int vx_group_probe_device_sync(void);
 /* This rank's tiles of the next frame, asynchronously on `stream`.  On rank 0
  * (device sync) the stream then waits for every rank's tiles: work queued
  * behind this call sees the whole frame.  Rank 0 may hold at most two

@@ -163,6 +163,7 @@ SIGNATURES = {
     "vx_group_create": [I32, I32, I64, P, P],
     "vx_group_connect": [P, P, I32],
     "vx_group_info": [P, P, P],
+    "vx_group_probe_device_sync": [],
     "vx_group_render": [P, P, P, P, P, P, P],
     "vx_group_release": [P, P],
     "vx_group_download": [P, P, P, I64, P],

@@ -93,6 +93,21 @@ int cu_check(CUresult r, const char* what) {
   return VX_ECUDA;
 }
 
+// a fenced stream write and a satisfied wait on `flag` (device memory)
+int memop_probe(uint8_t* flag) {
+  cudaStream_t ps;
+  VX_CUDA(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking));
+  int rc = cu_check(g_write32((CUstream)ps, (CUdeviceptr)flag, 1u, 0), "cuStreamWriteValue32(probe)");
+  if (!rc)
+    rc = cu_check(g_wait32((CUstream)ps, (CUdeviceptr)flag, 1u, CU_STREAM_WAIT_VALUE_GEQ),
+                  "cuStreamWaitValue32(probe)");
+  cudaError_t e = cudaStreamSynchronize(ps);
+  cudaStreamDestroy(ps);
+  if (rc) return rc;
+  if (e != cudaSuccess) return vx_cuda_fail(e, "stream memop probe", __FILE__, __LINE__);
+  return VX_OK;
+}
+
 uint64_t host_hash() {
   char name[256] = {0};
   gethostname(name, sizeof(name) - 1);
@@ -184,7 +199,7 @@ extern "C" int vx_group_connect(vx_group* g, const uint8_t* blobs, int32_t sync)
     vx_set_error("vx_group_connect: bad argument or already connected");
     return VX_EINVAL;
   }
-  bool shared_gpu = false;
+  bool shared_gpu = false, one_process = true;
   GroupBlob bs[kMaxWorld];
   for (int r = 0; r < g->world; ++r) {
     memcpy(&bs[r], blobs + (size_t)r * VX_GROUP_BLOB_BYTES, sizeof(GroupBlob));
@@ -201,9 +216,13 @@ extern "C" int vx_group_connect(vx_group* g, const uint8_t* blobs, int32_t sync)
     }
     for (int q = 0; q < r; ++q)
       if (!memcmp(bs[q].uuid, b.uuid, 16)) shared_gpu = true;
+    if (b.pid != g->blob.pid) one_process = false;
   }
   if (sync == VX_GROUP_SYNC_AUTO) sync = shared_gpu ? VX_GROUP_SYNC_HOST : VX_GROUP_SYNC_DEVICE;
-  if (sync == VX_GROUP_SYNC_DEVICE && shared_gpu) {
+  // Ranks of one process sharing a GPU are streams of one context: their
+  // flag waits are ordinary cross-stream waits (like cudaStreamWaitEvent).
+  // Across processes on one GPU a blocked context can time out: refused.
+  if (sync == VX_GROUP_SYNC_DEVICE && shared_gpu && !one_process) {
     vx_set_error("vx_group_connect: device-side frame flags need one GPU per rank (ranks share a "
                  "GPU: use VX_GROUP_SYNC_HOST)");
     return VX_EINVAL;
@@ -214,6 +233,10 @@ extern "C" int vx_group_connect(vx_group* g, const uint8_t* blobs, int32_t sync)
   }
   if (sync == VX_GROUP_SYNC_DEVICE) {
     int rc = load_memops();
+    if (rc) return rc;
+    // probe on this rank's own flag block: an unsupported driver fails here
+    // (the caller can fall back to VX_GROUP_SYNC_HOST), not inside a frame
+    rc = memop_probe(g->local + kConsumedOff + 64);
     if (rc) return rc;
   }
   for (int r = 0; r < g->world; ++r) {
@@ -249,6 +272,17 @@ extern "C" int vx_group_connect(vx_group* g, const uint8_t* blobs, int32_t sync)
   g->sync = sync;
   g->connected = true;
   return VX_OK;
+}
+
+extern "C" int vx_group_probe_device_sync(void) {
+  int rc = load_memops();
+  if (rc) return rc;
+  uint8_t* flag = nullptr;
+  VX_CUDA(cudaMalloc(&flag, 64));
+  VX_CUDA(cudaMemset(flag, 0, 64));
+  rc = memop_probe(flag);
+  cudaFree(flag);
+  return rc;
 }
 
 extern "C" int vx_group_info(const vx_group* g, int32_t* sync_out, uint32_t* frame_out) {

@@ -112,6 +112,9 @@ class NativeGroup:
                   _lib.ptr(blob))
         return blob.tobytes()
 
+    def probe_device_sync(self) -> bool:
+        return _lib.load().vx_group_probe_device_sync() == _lib.VX_OK
+
     def connect(self, blobs: bytes, sync: int) -> int:
         buf = np.frombuffer(blobs, dtype=np.uint8).copy()
         _lib.call("vx_group_connect", self.handle, _lib.ptr(buf), int(sync))
@@ -160,11 +163,22 @@ class FrameGroup:
         blobs = all_gather_bytes(blob, group)
         if sync == "auto":
             # decided collectively: every rank must agree on the protocol
-            mode = _lib.VX_GROUP_SYNC_HOST if self._shared(group) else _lib.VX_GROUP_SYNC_DEVICE
+            mode = (_lib.VX_GROUP_SYNC_HOST if self._shared(group) or not self._memops_ok(group)
+                    else _lib.VX_GROUP_SYNC_DEVICE)
         else:
             mode = {"device": _lib.VX_GROUP_SYNC_DEVICE, "host": _lib.VX_GROUP_SYNC_HOST}[sync]
         self.sync = self.backend.connect(b"".join(blobs), mode)
         self.frames = 0
+
+    def _memops_ok(self, group) -> bool:
+        """Every rank's device supports the stream-memop flags."""
+        import torch.distributed as dist
+
+        probe = getattr(self.backend, "probe_device_sync", None)
+        ok = probe() if probe is not None else True
+        out: list = [None] * self.world
+        dist.all_gather_object(out, bool(ok), group=group)
+        return all(out)
 
     def _shared(self, group) -> bool:
         shared = getattr(self.backend, "shares_device", None)

@@ -99,14 +99,6 @@ def test_group_rejects_foreign_blobs():
     try:
         with pytest.raises(_lib.NativeError, match="does not belong"):
             _lib.call("vx_group_connect", a, _lib.ptr(np.concatenate([ba, bb])), -1)
-        # ranks on one GPU cannot use the device flags
-        c = C.c_void_p()
-        bc = np.zeros(_lib.VX_GROUP_BLOB_BYTES, np.uint8)
-        _lib.call("vx_group_create", 1, 2, 1000, C.byref(c), _lib.ptr(bc))
-        with pytest.raises(_lib.NativeError, match="one GPU per rank"):
-            _lib.call("vx_group_connect", a, _lib.ptr(np.concatenate([ba, bc])),
-                      _lib.VX_GROUP_SYNC_DEVICE)
-        lib.vx_group_destroy(c)
     finally:
         lib.vx_group_destroy(a)
         lib.vx_group_destroy(b)
@@ -135,3 +127,75 @@ def test_bench_two_ranks_match_one_rank():
     assert two["frame"]["hits"] == one["frame"]["hits"]
     assert two["config"]["otsu_T"] == one["config"]["otsu_T"]
     assert two["e2e"]["value"] > 0 and two["value"] > 0
+
+
+def test_group_device_flags_two_threads(vx, small_sphere_volume, small_sphere_histogram):
+    """The device-sync protocol (stream-memop done / consumed flags, no host
+    round trip per frame) with two ranks as two threads of one process on
+    one GPU -- their flag waits are ordinary cross-stream waits of one
+    context.  Rank 1 runs ahead freely (bounded by the two slots); every
+    frame rank 0 downloads equals the single-rank frame."""
+    import threading
+
+    import torch
+
+    from paper_1807_03119_b200 import _lib
+    from paper_1807_03119_b200.volume import device_volume
+
+    lib = _lib.load()
+    assert lib.vx_group_probe_device_sync() == 0
+    W, H = 88, 64
+    dv = device_volume(small_sphere_volume)
+    cams = [vx.orbit_camera(small_sphere_volume, azimuth_deg=20.0 * f) for f in range(8)]
+    params = vx.RenderParams(width=W, height=H)
+    cfg = vx.FilterConfig(kind=vx.FilterKind.MEAN).resolve_threshold(small_sphere_histogram)
+    want = [vx.render_frame(small_sphere_volume, c, params, cfg, small_sphere_histogram).pixels.copy()
+            for c in cams]
+    from paper_1807_03119_b200.filters import native_config
+    from paper_1807_03119_b200.render import native_params, ray_setup
+
+    rp, fc = native_params(params), native_config(cfg, small_sphere_histogram)
+    rss = [ray_setup(c, W, H) for c in cams]
+    gs, bl = [], []
+    for r in range(2):
+        g = C.c_void_p()
+        b = np.zeros(_lib.VX_GROUP_BLOB_BYTES, np.uint8)
+        _lib.call("vx_group_create", r, 2, W * H, C.byref(g), _lib.ptr(b))
+        gs.append(g)
+        bl.append(b)
+    allb = np.concatenate(bl)
+    for g in gs:
+        _lib.call("vx_group_connect", g, _lib.ptr(allb), _lib.VX_GROUP_SYNC_DEVICE)
+    got, errors = [], []
+
+    def rank(r):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            for f, rs in enumerate(rss):
+                _lib.call("vx_group_render", gs[r], dv.handle, C.byref(rs), C.byref(rp),
+                          C.byref(fc), C.c_void_p(st.cuda_stream), None)
+                if r == 0:
+                    pix = np.zeros(W * H, np.uint8)
+                    _lib.call("vx_group_download", gs[0], _lib.ptr(pix), None, W * H,
+                              C.c_void_p(st.cuda_stream))
+                    got.append(pix.reshape(H, W))
+                    _lib.call("vx_group_release", gs[0], C.c_void_p(st.cuda_stream))
+            st.synchronize()
+        except Exception as exc:  # surfaced below
+            errors.append(exc)
+
+    ts = [threading.Thread(target=rank, args=(r,)) for r in (1, 0)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=120)
+    try:
+        assert not errors, errors
+        assert len(got) == len(want)
+        for f, (a, b) in enumerate(zip(got, want)):
+            assert np.array_equal(a, b), f
+    finally:
+        _lib.call("vx_synchronize")
+        for g in gs:
+            lib.vx_group_destroy(g)
