@@ -179,6 +179,19 @@ struct RenderArgs {
   const double* lut_host;  // host copy (map keys; never dereferenced on the device)
 };
 
+// Once-per-ray code (FP64 ray setup with its divisions, Sobel, Phong's FP64
+// pow) kept out of line, so the march loop's instructions stay resident in
+// the instruction cache (ncu: stall_no_instruction ~ as frequent as
+// long-scoreboard stalls with everything inlined).
+#ifndef VX_NOINLINE_COLD
+#define VX_NOINLINE_COLD 0  // measured: noinline costs an 808-byte stack frame and spills
+#endif
+#if VX_NOINLINE_COLD
+#define VX_COLD __device__ __noinline__
+#else
+#define VX_COLD __device__ __forceinline__
+#endif
+
 constexpr int kTileW = 8;
 constexpr int kTileH = 16;
 
@@ -460,7 +473,7 @@ __device__ __forceinline__ double filter_value(const VolView& V, const FiltD& F,
 // ---------------------------------------------------------------------------
 // ray setup (render.py:188-230)
 
-__device__ __forceinline__ void ray_dir(const RayCamD& C, int i, int j, double d[3]) {
+VX_COLD void ray_dir(const RayCamD& C, int i, int j, double d[3]) {
   const double u = __dmul_rn(
       __dmul_rn(__dsub_rn(__ddiv_rn(__dmul_rn(2.0, __dadd_rn((double)i, 0.5)), (double)C.W), 1.0),
                 C.tan_f),
@@ -485,7 +498,7 @@ __device__ __forceinline__ double nmax(double a, double b) {
   return (a != a || b != b) ? __longlong_as_double(0x7ff8000000000000ll) : (a > b ? a : b);
 }
 
-__device__ __forceinline__ void ray_span(const double o[3], const double d[3], int nx, int ny,
+VX_COLD void ray_span(const double o[3], const double d[3], int nx, int ny,
                                          int nz, double& t_enter, double& t_exit) {
   const double hi[3] = {__dsub_rn((double)nx, 0.5), __dsub_rn((double)ny, 0.5),
                         __dsub_rn((double)nz, 0.5)};
@@ -1108,7 +1121,7 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
 // Sobel (render.py:344-377) and Phong (render.py:385-403)
 
 template <bool CHECKED>
-__device__ void sobel(const VolView& V, long long x, long long y, long long z, const double fb[3],
+VX_COLD void sobel(const VolView& V, long long x, long long y, long long z, const double fb[3],
                       double n[3]) {
   int gx = 0, gy = 0, gz = 0;
 #pragma unroll
@@ -1138,7 +1151,7 @@ __device__ void sobel(const VolView& V, long long x, long long y, long long z, c
 // n.l follows the reference host's OpenBLAS dgemv (fma(n2,l2, fma(n0,l0, n1*l1)),
 // measured bit-exact on 20k random vectors); r.v follows numpy einsum
 // ((r0 v0 + r2 v2) + r1 v1).  See DESIGN.md "shading order".
-__device__ __forceinline__ double phong_intensity(const double n[3], const double v[3],
+VX_COLD double phong_intensity(const double n[3], const double v[3],
                                                   const ShadeD& S) {
   const double ndotl = __fma_rn(n[2], S.l[2], __fma_rn(n[0], S.l[0], __dmul_rn(n[1], S.l[1])));
   const double k2 = __dmul_rn(2.0, ndotl);
@@ -1332,7 +1345,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
     hit = st == kHit;
     if (hit) {
       voxel_at(R, a.M, ht, hx, hy, hz);
-      if (a.O.hit_value) hval = filter_value<KIND, CHECKED>(a.V, a.F, lut, hx, hy, hz);
+      // per-pixel diagnostics live in the DIAG kernel only (keeps a third
+      // inline copy of the filter out of the frame kernel's code)
+      if (DIAG && a.O.hit_value) hval = filter_value<KIND, CHECKED>(a.V, a.F, lut, hx, hy, hz);
     }
     // unbudgeted march: only a hit at or beyond the ray's own budget can
     // differ from the budgeted reference -> exact re-render by the host
@@ -1356,14 +1371,16 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
       pix = quantise(I);
     }
     a.O.pixels[p] = pix;
-    if (a.O.hit_voxel) {
-      a.O.hit_voxel[3 * p] = hit ? hx : -1;
-      a.O.hit_voxel[3 * p + 1] = hit ? hy : -1;
-      a.O.hit_voxel[3 * p + 2] = hit ? hz : -1;
+    if (DIAG) {
+      if (a.O.hit_voxel) {
+        a.O.hit_voxel[3 * p] = hit ? hx : -1;
+        a.O.hit_voxel[3 * p + 1] = hit ? hy : -1;
+        a.O.hit_voxel[3 * p + 2] = hit ? hz : -1;
+      }
+      if (a.O.hit_t) a.O.hit_t[p] = hit ? ht : 0.0f;
+      if (a.O.hit_value) a.O.hit_value[p] = hit ? hval : 0.0;
+      if (a.O.intensity) a.O.intensity[p] = I;
     }
-    if (a.O.hit_t) a.O.hit_t[p] = hit ? ht : 0.0f;
-    if (a.O.hit_value) a.O.hit_value[p] = hit ? hval : 0.0;
-    if (a.O.intensity) a.O.intensity[p] = I;
     pix_out = pix;
   }
   // warp-level aggregation (no block barrier: warps retire independently)
@@ -1379,7 +1396,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
     for (int i = 0; i < 8; ++i) {
       unsigned v = dg.c[i];
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0 && v) atomicAdd(a.O.diag + i, (unsigned long long)v);
+      if (lane == 0 && v && a.O.diag) atomicAdd(a.O.diag + i, (unsigned long long)v);
 #ifdef VX_WARP_TIMING
       const unsigned w = blockIdx.x * kWarpsPerBlock + (tid >> 5);
       if (lane == 0 && w < (1u << 20)) g_warp_diag[w * 9 + i] = v;
@@ -1746,9 +1763,14 @@ void launch_raycast(const RenderArgs& a, int grid, cudaStream_t s) {
   grid *= kBlocksPerTile;
   // unbudgeted launches reserve split_max extra blocks for split tiles
   const int grid_u = grid + (kSplitRays && a.tile_order ? a.split_max : 0);
-  if (a.M.explicit_max > 0)  // exact budget: user max_steps or the re-render
+  // per-pixel diagnostics (hit voxel / t / value / intensity, march counters)
+  // are written by the DIAG kernels only
+  const bool diag = a.O.diag || a.O.hit_voxel || a.O.hit_t || a.O.hit_value || a.O.intensity;
+  if (a.M.explicit_max > 0 && diag)  // exact budget: user max_steps or the re-render
+    raycast_kernel<KIND, CHECKED, true, true><<<grid, blk, 0, s>>>(a);
+  else if (a.M.explicit_max > 0)
     raycast_kernel<KIND, CHECKED, false, true><<<grid, blk, 0, s>>>(a);
-  else if (a.O.diag)
+  else if (diag)
     raycast_kernel<KIND, CHECKED, true, false><<<grid_u, blk, 0, s>>>(a);
   else if (!a.M.skip)  // full traversal (skipping off, or thr == 0): lean own-group loads
     raycast_kernel<KIND, CHECKED, false, false, false><<<grid_u, blk, 0, s>>>(a);
