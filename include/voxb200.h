@@ -124,6 +124,8 @@ typedef struct {
 /* ---- device / errors ---------------------------------------------------- */
 const char* vx_last_error(void);
 int vx_version(void);
+/* distance cap of the skip maps: level 0 = 8^3 bricks, else 4^3 cells */
+int vx_skip_cap(int32_t level);
 int vx_device_count(int* n_out);
 int vx_set_device(int device);
 int vx_synchronize(void);

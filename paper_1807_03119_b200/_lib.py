@@ -121,6 +121,7 @@ I32, I64, U64, F64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double
 SIGNATURES = {
     "vx_last_error": [],
     "vx_version": [],
+    "vx_skip_cap": [C.c_int32],
     "vx_device_count": [P],
     "vx_set_device": [C.c_int],
     "vx_synchronize": [],

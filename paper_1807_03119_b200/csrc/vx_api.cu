@@ -67,6 +67,7 @@ int vx_sm_count() {
 
 extern "C" const char* vx_last_error(void) { return tl_error; }
 extern "C" int vx_version(void) { return VX_VERSION; }
+extern "C" int vx_skip_cap(int32_t level) { return level == 0 ? VX_DIST_CAP : VX_FINE_CAP; }
 
 extern "C" int vx_device_count(int* n_out) {
   int n = 0;

@@ -33,7 +33,9 @@
 // (skips of up to 124 voxels per lookup; 17 MB at 1024^3, L2-resident).
 #define VX_CELL 4
 #define VX_CELL_SHIFT 2
+#ifndef VX_FINE_CAP
 #define VX_FINE_CAP 32
+#endif
 #define VX_DIST_CACHE 4
 
 // offset of voxel (x, y, z) & 7 inside its 8^3 brick

@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(4 * kSweepCols) dist_sweep_kernel(const uint8_
   const int n = AXIS == 1 ? my : mz;
   uint8_t* val = sweep_sm;                                   // [n][64] v, then D
   uint8_t* left = sweep_sm + (size_t)n * kSweepCols;         // [n][64] L
-  uint16_t* last = reinterpret_cast<uint16_t*>(sweep_sm + (size_t)2 * n * kSweepCols);  // [32][64]
+  uint16_t* last = reinterpret_cast<uint16_t*>(sweep_sm + (size_t)2 * n * kSweepCols);  // [cap][64]
   const int64_t stride = AXIS == 1 ? (int64_t)mx : (int64_t)mx * my;
   const int64_t base0 = AXIS == 1 ? (int64_t)blockIdx.y * mx * my : (int64_t)blockIdx.y * mx;
   const int x0 = blockIdx.x * kSweepCols;
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(4 * kSweepCols) dist_sweep_kernel(const uint8_
   if (tx < kSweepCols && x0 + tx < mx) {
     constexpr uint16_t kNone = 0xffffu;
     if (DIR <= 0) {  // left sweep
-      for (int w = 0; w < 32; ++w) last[w * kSweepCols + tx] = kNone;
+      for (int w = 0; w < cap; ++w) last[w * kSweepCols + tx] = kNone;
       int m = cap;
       for (int l = 0; l < n; ++l) {
         const int v = val[l * kSweepCols + tx];
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(4 * kSweepCols) dist_sweep_kernel(const uint8_
     } else {
       // right sweep, then D = min(L, R) (or R alone) in place of v (v(l) is
       // not read again)
-      for (int w = 0; w < 32; ++w) last[w * kSweepCols + tx] = kNone;
+      for (int w = 0; w < cap; ++w) last[w * kSweepCols + tx] = kNone;
       int m = cap;
       for (int l = n - 1; l >= 0; --l) {
         const int v = val[l * kSweepCols + tx];
@@ -365,12 +365,14 @@ static int dist_transform_dir(const uint8_t* maxmap, uint8_t* out, int mx, int m
       maxmap, out, mx, rows, thr, cap);
   VX_CHECK_LAUNCH();
   const unsigned gx = (unsigned)((mx + kSweepCols - 1) / kSweepCols);
-  // values >= cap never enter last[32]: the caps in use are 24 and 32
-  if (cap > 32) {
-    vx_set_error("distance cap %d > 32", cap);
+  // values >= cap never enter last[cap] (u8 maps: cap <= 255)
+  if (cap > 255) {
+    vx_set_error("distance cap %d > 255", cap);
     return VX_EINVAL;
   }
-  auto sweep_smem = [](int n) { return (size_t)2 * n * kSweepCols + 64 * kSweepCols; };
+  auto sweep_smem = [cap](int n) {
+    return (size_t)2 * n * kSweepCols + (size_t)2 * cap * kSweepCols;
+  };
   const size_t s1 = sweep_smem(my), s2 = sweep_smem(mz);
   if ((rc = smem_opt_in((const void*)dist_sweep_kernel<1, DY>, s1))) return rc;
   dist_sweep_kernel<1, DY><<<dim3(gx, (unsigned)mz), 4 * kSweepCols, s1, s>>>(out, tmp, mx, my,

@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 export VOXB200_NO_BUILD=1
 for v in "$@"; do
   export VOXB200_LIB=$PWD/paper_1807_03119_b200/libvoxb200$v.so
-  timeout 900 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_render.py tests/test_gpu_filters.py \
+  timeout 900 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_render.py tests/test_gpu_filters.py tests/test_gpu_volume.py \
     "tests/test_gpu_large.py::test_bench_frame_1024_full_vs_oracle" > gpurun_out/ab_tests$v.log 2>&1
   echo "lib$v tests rc=$? $(tail -1 gpurun_out/ab_tests$v.log)"
   timeout 600 python bench.py --steps 30 --warmup 5 --ncu off --no-cpu --orbit 0 --noskip-steps 5 \
