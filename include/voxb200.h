@@ -124,8 +124,6 @@ typedef struct {
 /* ---- device / errors ---------------------------------------------------- */
 const char* vx_last_error(void);
 int vx_version(void);
-/* distance cap of the skip maps: level 0 = 8^3 bricks, else 4^3 cells */
-int vx_skip_cap(int32_t level);
 int vx_device_count(int* n_out);
 int vx_set_device(int device);
 int vx_synchronize(void);
@@ -160,6 +158,9 @@ int vx_volume_destroy(vx_volume* vol);
 int vx_volume_dims(const vx_volume* vol, int64_t dims_out[3]);
 int vx_volume_read(const vx_volume* vol, uint8_t* host_out); /* compact copy back */
 int vx_volume_device_bytes(const vx_volume* vol, uint64_t* bytes_out);
+/* distance cap of the volume's skip maps: level 0 = 8^3 bricks, else the 4^3
+ * cell maps (grows with the volume: 32 cells up to 512^3 ... 128 at 2048^3) */
+int vx_volume_skip_cap(const vx_volume* vol, int32_t level, int32_t* cap_out);
 
 /* ---- statistics (histogram.py:59-133, metrics.py:26-33) ------------------ */
 /* K1: counts of the volume's voxels (cached at creation). */

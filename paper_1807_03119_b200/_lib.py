@@ -121,7 +121,6 @@ I32, I64, U64, F64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double
 SIGNATURES = {
     "vx_last_error": [],
     "vx_version": [],
-    "vx_skip_cap": [C.c_int32],
     "vx_device_count": [P],
     "vx_set_device": [C.c_int],
     "vx_synchronize": [],
@@ -134,6 +133,7 @@ SIGNATURES = {
     "vx_volume_dims": [P, P],
     "vx_volume_read": [P, P],
     "vx_volume_device_bytes": [P, P],
+    "vx_volume_skip_cap": [P, C.c_int32, P],
     "vx_histogram": [P, P],
     "vx_histogram_host": [P, U64, P],
     "vx_histogram_device": [P, U64, P, P],

@@ -67,7 +67,6 @@ int vx_sm_count() {
 
 extern "C" const char* vx_last_error(void) { return tl_error; }
 extern "C" int vx_version(void) { return VX_VERSION; }
-extern "C" int vx_skip_cap(int32_t level) { return level == 0 ? VX_DIST_CAP : VX_FINE_CAP; }
 
 extern "C" int vx_device_count(int* n_out) {
   int n = 0;
@@ -183,6 +182,7 @@ int vx_volume_alloc(int64_t nx, int64_t ny, int64_t nz, vx_volume** out) {
   v->csy = v->ncx + 2;
   v->csz = (int64_t)(v->ncx + 2) * (v->ncy + 2);
   v->cmap_bytes = (uint64_t)v->csz * (v->ncz + 2);
+  v->fine_cap = vx_fine_cap_for(nx, ny, nz);
   cudaError_t e = cudaEventCreateWithFlags(&v->scratch_done, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     delete v;
@@ -417,6 +417,15 @@ extern "C" int vx_volume_destroy(vx_volume* v) {
   if (v->bricks) cudaFree(v->bricks);
   if (cur != v->device) cudaSetDevice(cur);
   delete v;
+  return VX_OK;
+}
+
+extern "C" int vx_volume_skip_cap(const vx_volume* v, int32_t level, int32_t* cap_out) {
+  if (!v || !cap_out) {
+    vx_set_error("vx_volume_skip_cap: null argument");
+    return VX_EINVAL;
+  }
+  *cap_out = level == 0 ? VX_DIST_CAP : v->fine_cap;
   return VX_OK;
 }
 

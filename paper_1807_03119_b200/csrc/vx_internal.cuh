@@ -29,13 +29,23 @@
 #define VX_BRICK_SHIFT 3
 // Chebyshev brick-distance cap of the coarse exact-skip map (8^3 bricks).
 #define VX_DIST_CAP 24
-// Fine exact-skip map: 4^3 cells, Chebyshev cell distance capped at 32
-// (skips of up to 124 voxels per lookup; 17 MB at 1024^3, L2-resident).
+// Fine exact-skip map: 4^3 cells, Chebyshev cell distance capped at a
+// per-volume cap (17 MB at 1024^3, L2-resident).  Long skips step over whole
+// chunks by the exact base recurrence (one FP32 add per 16 samples), so the
+// best cap grows with the volume: 32 cells up to 512^3, 64 at 1024^3, 128
+// from 2048^3 (profiles/r2/r2_ab_skip_cap.txt); VX_FINE_CAP > 0 forces one.
 #define VX_CELL 4
 #define VX_CELL_SHIFT 2
 #ifndef VX_FINE_CAP
-#define VX_FINE_CAP 32
+#define VX_FINE_CAP 0
 #endif
+static inline int vx_fine_cap_for(int64_t nx, int64_t ny, int64_t nz) {
+  if (VX_FINE_CAP > 0) return VX_FINE_CAP;
+  int64_t m = nx > ny ? nx : ny;
+  m = m > nz ? m : nz;
+  const int64_t c = m / 16;
+  return (int)(c < 32 ? 32 : (c > 128 ? 128 : c));
+}
 #define VX_DIST_CACHE 4
 
 // offset of voxel (x, y, z) & 7 inside its 8^3 brick
@@ -176,6 +186,7 @@ struct vx_volume {
   // cell (4^3) max map with a 1-cell apron: dims (ncx+2, ncy+2, ncz+2)
   uint8_t* cmax;
   int ncx, ncy, ncz;
+  int fine_cap;  // distance cap of the cell maps (vx_fine_cap_for)
   int64_t csy, csz;
   uint64_t cmap_bytes;
   DistEntry dist[VX_DIST_CACHE];

@@ -396,12 +396,12 @@ int vx_launch_dist_map(const vx_volume* v, int thr, uint8_t* map, cudaStream_t s
                           v->scratch + v->cmap_bytes, s);
   if (rc) return rc;
   return dist_transform(v->cmax, map + v->map_bytes, v->ncx + 2, v->ncy + 2, v->ncz + 2, thr,
-                        VX_FINE_CAP, v->scratch + v->cmap_bytes, s);
+                        v->fine_cap, v->scratch + v->cmap_bytes, s);
 }
 
 int vx_launch_dist_cells(const vx_volume* v, const uint8_t* occ, uint8_t* out, int thr,
                          cudaStream_t s) {
-  return dist_transform(occ, out, v->ncx + 2, v->ncy + 2, v->ncz + 2, thr, VX_FINE_CAP,
+  return dist_transform(occ, out, v->ncx + 2, v->ncy + 2, v->ncz + 2, thr, v->fine_cap,
                         v->scratch + v->cmap_bytes, s);
 }
 
@@ -415,7 +415,7 @@ int vx_launch_dist_cells_oct(const vx_volume* v, const uint8_t* occ, uint8_t* ou
   const int mx = v->ncx + 2, my = v->ncy + 2, mz = v->ncz + 2;
   uint8_t* tmp = v->scratch + v->cmap_bytes;
 #define VX_OCT(o, dx, dy, dz) \
-  case o: return dist_transform_dir<dx, dy, dz>(occ, out, mx, my, mz, thr, VX_FINE_CAP, tmp, s)
+  case o: return dist_transform_dir<dx, dy, dz>(occ, out, mx, my, mz, thr, v->fine_cap, tmp, s)
   switch (oct) {
     VX_OCT(0, 1, 1, 1);
     VX_OCT(1, -1, 1, 1);
@@ -426,7 +426,7 @@ int vx_launch_dist_cells_oct(const vx_volume* v, const uint8_t* occ, uint8_t* ou
     VX_OCT(6, 1, -1, -1);
     VX_OCT(7, -1, -1, -1);
     default:
-      return dist_transform(occ, out, mx, my, mz, thr, VX_FINE_CAP, tmp, s);
+      return dist_transform(occ, out, mx, my, mz, thr, v->fine_cap, tmp, s);
   }
 #undef VX_OCT
 }

@@ -170,9 +170,7 @@ def test_distance_map_long_lines(vx):
     data[150:160, 20:30, 100:240] = 180
     data[5, 250, :] = 255
     dv = device_volume(vx.Volume(dims=(nx, ny, nz), data=data))
-    from paper_1807_03119_b200 import _lib
-
-    caps = {lv: _lib.load().vx_skip_cap(lv) for lv in (0, 1)}
+    caps = {lv: dv.skip_cap(lv) for lv in (0, 1)}
     for c, cap, level in ((4, caps[1], 1), (8, caps[0], 0)):
         ncz, ncy, ncx = (nz + c - 1) // c, (ny + c - 1) // c, (nx + c - 1) // c
         pad = np.zeros((ncz * c, ncy * c, ncx * c), dtype=np.uint8)
@@ -202,9 +200,7 @@ def test_distance_map_is_exact_chebyshev(vx):
     bmax = pad.reshape(nbz, 8, nby, 8, nbx, 8).max(axis=(1, 3, 5))
     occ = np.zeros((nbz + 2, nby + 2, nbx + 2), dtype=bool)
     occ[1:-1, 1:-1, 1:-1] = bmax >= 100
-    from paper_1807_03119_b200 import _lib
-
-    want = _brute_distance(occ, _lib.load().vx_skip_cap(0))
+    want = _brute_distance(occ, dv.skip_cap(0))
     assert np.array_equal(dm, want)
     # fine level: 4^3 cells, cap 32
     fm = dv.distance_map(100, level=1).astype(np.int64)
@@ -215,7 +211,7 @@ def test_distance_map_is_exact_chebyshev(vx):
     cmax = pad2.reshape(ncz, c, ncy, c, ncx, c).max(axis=(1, 3, 5))
     occ2 = np.zeros((ncz + 2, ncy + 2, ncx + 2), dtype=bool)
     occ2[1:-1, 1:-1, 1:-1] = cmax >= 100
-    assert np.array_equal(fm, _brute_distance(occ2, _lib.load().vx_skip_cap(1)))
+    assert np.array_equal(fm, _brute_distance(occ2, dv.skip_cap(1)))
 
 
 def _brute_orthant(occ: np.ndarray, cap: int, oct: int) -> np.ndarray:
@@ -252,11 +248,36 @@ def test_orthant_maps_exact(vx):
     cmax = pad.reshape(ncz, c, ncy, c, ncx, c).max(axis=(1, 3, 5))
     occ = np.zeros((ncz + 2, ncy + 2, ncx + 2), dtype=bool)
     occ[1:-1, 1:-1, 1:-1] = cmax >= 100
-    from paper_1807_03119_b200 import _lib
-
     iso = dv.distance_map(100, level=1).astype(np.int64)
     for o in range(8):
         got = dv.distance_map(100, level=8 + o).astype(np.int64)
-        want = _brute_orthant(occ, _lib.load().vx_skip_cap(1), o)
+        want = _brute_orthant(occ, dv.skip_cap(1), o)
         assert np.array_equal(got, want), o
         assert np.all(got >= iso)  # one-sided: never shorter than the two-sided map
+
+
+def test_long_volume_uses_a_larger_cap_exactly(vx):
+    """A 2100-voxel-long volume gets the 128-cell cap (vx_fine_cap_for): its
+    two-sided and orthant maps are still the exact capped distances."""
+    from paper_1807_03119_b200.volume import device_volume
+
+    rs = np.random.default_rng(11)
+    nz, ny, nx = 2100, 12, 10
+    data = rs.integers(0, 40, (nz, ny, nx), dtype=np.uint8)
+    for z in (3, 700, 1500, 2099):
+        data[z, rs.integers(0, ny), rs.integers(0, nx)] = 240
+    dv = device_volume(vx.Volume(dims=(nx, ny, nz), data=data))
+    cap = dv.skip_cap(1)
+    assert cap == 128
+    c = 4
+    ncz, ncy, ncx = (nz + c - 1) // c, (ny + c - 1) // c, (nx + c - 1) // c
+    pad = np.zeros((ncz * c, ncy * c, ncx * c), dtype=np.uint8)
+    pad[:nz, :ny, :nx] = data
+    cmax = pad.reshape(ncz, c, ncy, c, ncx, c).max(axis=(1, 3, 5))
+    occ = np.zeros((ncz + 2, ncy + 2, ncx + 2), dtype=bool)
+    occ[1:-1, 1:-1, 1:-1] = cmax >= 100
+    assert np.array_equal(dv.distance_map(100, level=1).astype(np.int64),
+                          _brute_distance(occ, cap).clip(max=cap))
+    for o in (0, 4, 7):
+        assert np.array_equal(dv.distance_map(100, level=8 + o).astype(np.int64),
+                              _brute_orthant(occ, cap, o)), o
