@@ -49,10 +49,16 @@ class Camera:
     def __post_init__(self):
         if not 0.0 < self.fov_y_deg < 180.0:
             raise RenderError(f"fov must be in (0, 180), got {self.fov_y_deg}")
-        self.basis()
+        # validated and kept: a moving camera is a new Camera per frame, and
+        # ray_setup would otherwise recompute the basis (numpy, ~15 us)
+        object.__setattr__(self, "_basis", self._compute_basis())
 
     def basis(self) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
         """Orthonormal (right, up, forward), numpy FP64 (render.py:49-62)."""
+        right, up, fwd = self.__dict__["_basis"]
+        return right.copy(), up.copy(), fwd.copy()
+
+    def _compute_basis(self) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
         pos = np.asarray(self.position, dtype=np.float64)
         fwd = np.asarray(self.look_at, dtype=np.float64) - pos
         norm = np.linalg.norm(fwd)
@@ -164,15 +170,14 @@ class Hit:
 
 def ray_setup(camera: Camera, width: int, height: int) -> _lib.vx_ray_setup:
     """Host FP64 constants of primary_ray_dirs (render.py:190-192)."""
-    right, up, fwd = camera.basis()
+    right, up, fwd = camera.__dict__["_basis"]
     rs = _lib.vx_ray_setup()
-    for i in range(3):
-        rs.right[i] = float(right[i])
-        rs.up[i] = float(up[i])
-        rs.fwd[i] = float(fwd[i])
-        rs.origin[i] = float(camera.position[i])
-    rs.tan_f = math.tan(math.radians(camera.fov_y_deg) / 2.0)
-    rs.aspect = width / height
+    # right, up, fwd, origin, tan_f, aspect: 14 contiguous doubles
+    d = np.frombuffer(rs, dtype=np.float64, count=14)
+    d[0:3], d[3:6], d[6:9] = right, up, fwd
+    d[9:12] = camera.position
+    d[12] = math.tan(math.radians(camera.fov_y_deg) / 2.0)
+    d[13] = width / height
     rs.width = width
     rs.height = height
     return rs
