@@ -8,7 +8,7 @@
 namespace {
 
 #ifdef VX_HIST_TIMING
-__device__ unsigned long long g_ht[8];
+__device__ unsigned long long g_ht[16];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -18,8 +18,22 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #else
 #define VX_HT(k) do {} while (0)
 #endif
+#ifdef VX_HIST_TIMING
+// block-level marks: [8] first block start (min), [9] last counting done
+// (max), [10] last merge + global atomics done (max), [11] first block end
+#define VX_HTMIN(k) do { if (threadIdx.x == 0) atomicMin(&g_ht[k], gtimer()); } while (0)
+#define VX_HTMAX(k) do { if (threadIdx.x == 0) atomicMax(&g_ht[k], gtimer()); } while (0)
+#else
+#define VX_HTMIN(k) do {} while (0)
+#define VX_HTMAX(k) do {} while (0)
+#endif
 
 constexpr int kHistThreads = 512;
+// K2 as a PDL-launched second kernel with a warm-up pass (below): measured
+// no faster than the fused last-block tail (512^3 35.8 vs 35.7 us), off
+#ifndef VX_HIST_PDL
+#define VX_HIST_PDL 0
+#endif
 constexpr int kHistBlocksPerSM = 4;
 
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
@@ -35,17 +49,43 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
 // (CT volumes are dominated by a background spike; a per-warp [bin] table
 // would serialise on it).
 __device__ __forceinline__ void count_word(uint32_t* lane_base, uint32_t w) {
-  atomicAdd(lane_base + ((w & 0xffu) << 5), 1u);
-  atomicAdd(lane_base + (((w >> 8) & 0xffu) << 5), 1u);
-  atomicAdd(lane_base + (((w >> 16) & 0xffu) << 5), 1u);
-  atomicAdd(lane_base + ((w >> 24) << 5), 1u);
+  // byte k isolated by one PRMT, then address = lane_base + 32*byte (one
+  // IMAD): 3 instructions per byte with the atomic, where shift + mask + add
+  // took 4 -- the count loop is issue-bound below ~1 GB (ncu at 512^3:
+  // issue active 71 %, "not selected" the top stall)
+  atomicAdd(lane_base + (__byte_perm(w, 0u, 0x4440u) << 5), 1u);
+  atomicAdd(lane_base + (__byte_perm(w, 0u, 0x4441u) << 5), 1u);
+  atomicAdd(lane_base + (__byte_perm(w, 0u, 0x4442u) << 5), 1u);
+  atomicAdd(lane_base + (__byte_perm(w, 0u, 0x4443u) << 5), 1u);
 }
 
 // Counts this block's share of data[0, n) into the [bin][lane] shared table
 // `sh` (zeroed here) and reduces it to per-bin block totals tot[256].
+__device__ __forceinline__ void count_vec4(uint32_t* lane_base, const uint4& a, const uint4& b,
+                                           const uint4& c, const uint4& d) {
+  count_word(lane_base, a.x); count_word(lane_base, a.y);
+  count_word(lane_base, a.z); count_word(lane_base, a.w);
+  count_word(lane_base, b.x); count_word(lane_base, b.y);
+  count_word(lane_base, b.z); count_word(lane_base, b.w);
+  count_word(lane_base, c.x); count_word(lane_base, c.y);
+  count_word(lane_base, c.z); count_word(lane_base, c.w);
+  count_word(lane_base, d.x); count_word(lane_base, d.y);
+  count_word(lane_base, d.z); count_word(lane_base, d.w);
+}
+
+// next != nullptr: blocks take 4*blockDim.x-vector chunks (32 KB) from the
+// counter *next (zeroed before the launch) instead of a fixed grid-stride
+// share.  Measured with %globaltimer marks: with fixed shares the first
+// block finished counting at 18.5 us and the last at 27.1 us (512^3; 136 vs
+// 187 us at 1024^3) -- SMs see unequal bandwidth -- so the kernel ended
+// with the slowest SM's share.  The next chunk's index is fetched while the
+// current chunk's loads are in flight.
 __device__ __forceinline__ void hist_block_local(const uint8_t* __restrict__ data, uint64_t n,
-                                                 uint32_t* sh, uint32_t* tot) {
+                                                 uint32_t* sh, uint32_t* tot,
+                                                 unsigned int* next = nullptr) {
+  __shared__ unsigned int chunk_idx[2];
   for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) sh[i] = 0u;
+  if (next && threadIdx.x == 0) chunk_idx[0] = atomicAdd(next, 1u);
   __syncthreads();
 
   const uint32_t lane = threadIdx.x & 31u;
@@ -65,6 +105,34 @@ __device__ __forceinline__ void hist_block_local(const uint8_t* __restrict__ dat
   if (tid < head) atomicAdd(lane_base + ((uint32_t)data[tid] << 5), 1u);
   if (tid < n - tail_start) atomicAdd(lane_base + ((uint32_t)data[tail_start + tid] << 5), 1u);
 
+  if (next) {
+    const uint64_t bd = blockDim.x, ch = 4 * bd;
+    int p = 0;
+    for (;;) {
+      const uint64_t c0 = (uint64_t)chunk_idx[p] * ch;
+      if (c0 >= nvec) break;
+      if (threadIdx.x == 0) chunk_idx[p ^ 1] = atomicAdd(next, 1u);
+      const uint64_t j = c0 + threadIdx.x;
+      if (c0 + ch <= nvec) {
+        const uint4 a = ld_stream(vec + j), b = ld_stream(vec + j + bd),
+                    c = ld_stream(vec + j + 2 * bd), d = ld_stream(vec + j + 3 * bd);
+        count_vec4(lane_base, a, b, c, d);
+      } else {  // the last, partial chunk
+        const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+        uint4 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = j + k * bd < nvec ? ld_stream(vec + j + k * bd) : z;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (j + k * bd < nvec) {
+            count_word(lane_base, v[k].x); count_word(lane_base, v[k].y);
+            count_word(lane_base, v[k].z); count_word(lane_base, v[k].w);
+          }
+      }
+      __syncthreads();  // chunk_idx[p ^ 1] published; chunk_idx[p] free again
+      p ^= 1;
+    }
+  } else {
   // body: 4 x 16 B in flight per thread
   uint64_t i = tid;
   for (; i + 3 * nthreads < nvec; i += 4 * nthreads) {
@@ -72,14 +140,7 @@ __device__ __forceinline__ void hist_block_local(const uint8_t* __restrict__ dat
     uint4 b = ld_stream(vec + i + nthreads);
     uint4 c = ld_stream(vec + i + 2 * nthreads);
     uint4 d = ld_stream(vec + i + 3 * nthreads);
-    count_word(lane_base, a.x); count_word(lane_base, a.y);
-    count_word(lane_base, a.z); count_word(lane_base, a.w);
-    count_word(lane_base, b.x); count_word(lane_base, b.y);
-    count_word(lane_base, b.z); count_word(lane_base, b.w);
-    count_word(lane_base, c.x); count_word(lane_base, c.y);
-    count_word(lane_base, c.z); count_word(lane_base, c.w);
-    count_word(lane_base, d.x); count_word(lane_base, d.y);
-    count_word(lane_base, d.z); count_word(lane_base, d.w);
+    count_vec4(lane_base, a, b, c, d);
   }
   // remainder (< 4 vectors per thread): loads issued together, so a thread
   // waits on one memory round trip instead of up to three in a row
@@ -98,7 +159,10 @@ __device__ __forceinline__ void hist_block_local(const uint8_t* __restrict__ dat
       }
     }
   }
+  }  // static shares
   __syncthreads();
+  VX_HTMAX(9);
+  VX_HTMIN(11);
 
   // merge the 32 lane columns of each bin (rotated to stay conflict-free)
   for (int b = threadIdx.x; b < 256; b += blockDim.x) {
@@ -112,8 +176,10 @@ __device__ __forceinline__ void hist_block_local(const uint8_t* __restrict__ dat
 // Block-local histogram, then the block's 256 totals into out[256] (u64
 // atomics; a DSMEM pre-merge across 2/4/8-block clusters measured no faster).
 __device__ __forceinline__ void hist_block(const uint8_t* __restrict__ data, uint64_t n,
-                                           uint32_t* sh, uint32_t* tot, unsigned long long* out) {
-  hist_block_local(data, n, sh, tot);
+                                           uint32_t* sh, uint32_t* tot, unsigned long long* out,
+                                           unsigned int* next = nullptr) {
+  VX_HTMIN(8);
+  hist_block_local(data, n, sh, tot, next);
   __syncthreads();
   for (int b = threadIdx.x; b < 256; b += blockDim.x)
     if (tot[b]) atomicAdd(out + b, (unsigned long long)tot[b]);
@@ -372,16 +438,19 @@ __global__ void __launch_bounds__(256) otsu_kernel(const unsigned long long* __r
 struct HistWs {
   unsigned long long bins[256];
   unsigned int ticket;
+  unsigned int next;  // chunk counter of the dynamic shares
 };
 
 __global__ void __launch_bounds__(kHistThreads, kHistBlocksPerSM)
 hist_otsu_kernel(const uint8_t* __restrict__ data, uint64_t n, HistWs* __restrict__ ws,
-                 unsigned long long* __restrict__ counts_out, int32_t* __restrict__ T_out) {
+                 unsigned long long* __restrict__ counts_out, int32_t* __restrict__ T_out,
+                 int dynamic) {
   static_assert(sizeof(OtsuSmem) <= 256 * 32 * 4, "Otsu scratch must fit the histogram table");
   __shared__ __align__(16) uint32_t sh[256 * 32];
   __shared__ uint32_t tot[256];
   __shared__ bool last;
-  hist_block(data, n, sh, tot, ws->bins);
+  hist_block(data, n, sh, tot, ws->bins, dynamic ? &ws->next : nullptr);
+  VX_HTMAX(10);
   // the block's bin atomics precede thread 0's fence (barrier), which
   // precedes its ticket; one fencing thread per block, as in the CUDA
   // guide's last-block reduction.  The last block's tail (bins, scan,
@@ -407,7 +476,10 @@ hist_otsu_kernel(const uint8_t* __restrict__ data, uint64_t n, HistWs* __restric
     counts_out[threadIdx.x] = c;
     ws->bins[threadIdx.x] = 0ull;
   }
-  if (threadIdx.x == 0) ws->ticket = 0u;
+  if (threadIdx.x == 0) {
+    ws->ticket = 0u;
+    ws->next = 0u;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -481,6 +553,39 @@ __global__ void sub_bin0_kernel(unsigned long long* counts, unsigned long long v
   counts[0] -= v;
 }
 
+// K1 + K2 as two kernels with programmatic dependent launch
+// (VX_HIST_PDL): the counting grid lets its dependent launch at once; the
+// Otsu block, scheduled as soon as a counting block retires, first runs the
+// scan on a dummy histogram -- its SM's instruction caches warm while the
+// counting finishes (the fused kernel's last block executed that code cold:
+// ~3.5 us for the warp scans alone, %globaltimer marks) -- then waits for the
+// counting grid (griddepcontrol.wait: completion + memory flush) and scans
+// the real bins.
+__global__ void __launch_bounds__(kHistThreads, kHistBlocksPerSM)
+hist_count_kernel(const uint8_t* __restrict__ data, uint64_t n, HistWs* __restrict__ ws,
+                  int dynamic) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  __shared__ __align__(16) uint32_t sh[256 * 32];
+  __shared__ uint32_t tot[256];
+  hist_block(data, n, sh, tot, ws->bins, dynamic ? &ws->next : nullptr);
+}
+
+__global__ void __launch_bounds__(256) otsu_tail_kernel(HistWs* __restrict__ ws,
+                                                        unsigned long long* __restrict__ counts_out,
+                                                        int32_t* __restrict__ T_out) {
+  __shared__ OtsuSmem S;
+  __shared__ int32_t dummy_T;
+  // warm-up on a synthetic histogram (every path: scan, screen, exact compare)
+  otsu_block(1ull + (threadIdx.x % 7u), S, &dummy_T);
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const unsigned long long c = __ldcg(ws->bins + threadIdx.x);
+  otsu_block(c, S, T_out);
+  counts_out[threadIdx.x] = c;
+  ws->bins[threadIdx.x] = 0ull;
+  if (threadIdx.x == 0) ws->next = 0u;
+}
+
 }  // namespace
 
 int vx_launch_hist(const uint8_t* dev, uint64_t n, uint64_t* dev_counts, cudaStream_t s) {
@@ -529,15 +634,39 @@ int vx_launch_hist_otsu(const uint8_t* dev, uint64_t n, uint64_t* dev_counts, in
   uint64_t want = (n / 16 + kHistThreads - 1) / kHistThreads;
   uint64_t grid = (uint64_t)sms * kHistBlocksPerSM;
   if (want < grid) grid = want ? want : 1;
-  hist_otsu_kernel<<<(unsigned)grid, kHistThreads, 0, s>>>(
-      dev, n, ws, reinterpret_cast<unsigned long long*>(dev_counts), dev_T);
+  // dynamic 32 KB shares from 512 MiB up: 1024^3 190 -> 184 us, 2048^3
+  // 1.44 -> 1.36 ms; below, the per-chunk barriers cost more than the
+  // imbalance (512^3 35.3 -> 36.9 us)
+  const int dynamic = n >= (1ull << 29) ? 1 : 0;
+#if VX_HIST_PDL
+  hist_count_kernel<<<(unsigned)grid, kHistThreads, 0, s>>>(dev, n, ws, dynamic);
   VX_CHECK_LAUNCH();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  VX_CUDA(cudaLaunchKernelEx(&cfg, otsu_tail_kernel, ws,
+                             reinterpret_cast<unsigned long long*>(dev_counts), dev_T));
+  VX_CHECK_LAUNCH();
+#else
+  hist_otsu_kernel<<<(unsigned)grid, kHistThreads, 0, s>>>(
+      dev, n, ws, reinterpret_cast<unsigned long long*>(dev_counts), dev_T, dynamic);
+  VX_CHECK_LAUNCH();
+#endif
   return VX_OK;
 }
 
 #ifdef VX_HIST_TIMING
 extern "C" int vx_debug_hist_times(unsigned long long* out) {
-  VX_CUDA(cudaMemcpyFromSymbol(out, g_ht, 8 * 8));
+  VX_CUDA(cudaMemcpyFromSymbol(out, g_ht, 16 * 8));
+  unsigned long long init[16];
+  for (int i = 0; i < 16; ++i) init[i] = (i == 8 || i == 11) ? ~0ull : 0ull;
+  VX_CUDA(cudaMemcpyToSymbol(g_ht, init, 16 * 8));
   return VX_OK;
 }
 #endif
