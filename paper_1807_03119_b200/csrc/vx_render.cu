@@ -1484,9 +1484,16 @@ __device__ __forceinline__ int cost_bucket(unsigned c) {
   return b > 63 ? 63 : b;
 }
 
+// A moving camera (rx, ry > 0: the image-space motion between the frames
+// whose costs are used, in tiles) orders and splits by the costs dilated
+// over that neighbourhood (max filter), so a heavy region that moved one or
+// two tiles is still started first and split; the frame-length estimate
+// (total) stays the undilated sum.  dil: n words of scratch.
 __global__ void __launch_bounds__(1024) tile_order_kernel(uint32_t* __restrict__ cost,
                                                           uint32_t* __restrict__ order, int n,
-                                                          int split_us, int slots) {
+                                                          int split_us, int slots, int tiles_x,
+                                                          int rx, int ry,
+                                                          uint32_t* __restrict__ dil) {
   __shared__ unsigned cnt[64];
   __shared__ unsigned long long total;
   __shared__ unsigned top;
@@ -1496,13 +1503,35 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(uint32_t* __restrict__
     total = 0;
     top = 0;
   }
+  unsigned long long raw_total = 0;
+  const uint32_t* cc = cost;
+  if (rx > 0 || ry > 0) {
+    const int tiles_y = (n + tiles_x - 1) / tiles_x;
+    for (int i = tid; i < n; i += blockDim.x) {
+      const int tx = i % tiles_x, ty = i / tiles_x;
+      unsigned m = 0;
+      for (int dy = -ry; dy <= ry; ++dy) {
+        const int y = ty + dy;
+        if (y < 0 || y >= tiles_y) continue;
+        for (int dx = -rx; dx <= rx; ++dx) {
+          const int x = tx + dx;
+          const int j = y * tiles_x + x;
+          if (x >= 0 && x < tiles_x && j < n) m = max(m, cost[j]);
+        }
+      }
+      dil[i] = m;
+      raw_total += cost[i];
+    }
+    cc = dil;
+  }
   __syncthreads();
-  unsigned long long my_total = 0;
+  const bool dilated = cc != cost;
+  unsigned long long my_total = raw_total;  // the frame-length estimate: undilated
   unsigned my_top = 0;
   for (int i = tid; i < n; i += blockDim.x) {
-    const unsigned c = cost[i];
+    const unsigned c = cc[i];
     atomicAdd(&cnt[cost_bucket(c)], 1u);
-    my_total += c;
+    if (!dilated) my_total += c;
     my_top = max(my_top, c);
   }
   for (int o = 16; o > 0; o >>= 1) {
@@ -1544,7 +1573,7 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(uint32_t* __restrict__
   }
   __syncthreads();
   for (int i = tid; i < n; i += blockDim.x) {
-    order[atomicAdd(&cnt[cost_bucket(cost[i])], 1u)] = (uint32_t)i;
+    order[atomicAdd(&cnt[cost_bucket(cc[i])], 1u)] = (uint32_t)i;
     cost[i] = 0;
   }
 }
@@ -1970,6 +1999,15 @@ static double trace_us() {
     }                                                                             \
   } while (0)
 
+// Cost dilation of the tile order for a moving camera; VOXB200_DILATE=0 off
+static bool dilate_moving() {
+  static const bool on = [] {
+    const char* e = getenv("VOXB200_DILATE");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
 // Orthant skip maps: VOXB200_ORTHANT=0 renders on the
 // two-sided Chebyshev maps only
 static bool orthant_maps_on() {
@@ -2160,6 +2198,8 @@ struct TileSched {
   cudaStream_t side = nullptr;  // ordering kernels
   cudaEvent_t costs_done[2] = {nullptr, nullptr}, order_done[2] = {nullptr, nullptr};
   int device = -1;
+  vx_ray_setup last_rs[2];  // camera of the frame that recorded costs into buf[p]
+  bool have_rs[2] = {false, false};
 };
 static thread_local TileSched tl_sched;
 
@@ -2241,12 +2281,14 @@ static int tile_sched(vx_volume* vol, const vx_ray_setup* rs, int rank, int worl
         t.buf[p] = nullptr;
       }
       // stream-ordered pool (no device-wide cudaMalloc inside a frame)
-      VX_CUDA(vx_malloc_async(&t.buf[p], (size_t)grid * 8 + 4 * kSchedHdr, s));
+      // order[grid], header, cost[grid], dilated cost[grid]
+      VX_CUDA(vx_malloc_async(&t.buf[p], (size_t)grid * 12 + 4 * kSchedHdr, s));
       if (!t.demand[p]) t.demand[p] = demand_slot();
       if (!t.demand[p]) VX_CUDA(cudaHostAlloc(&t.demand[p], 4 * kSchedHdr, cudaHostAllocDefault));
       for (int k = 0; k < kSchedHdr; ++k) t.demand[p][k] = 0;
       VX_CUDA(cudaMemsetAsync(t.buf[p] + grid + kSchedHdr, 0, (size_t)grid * 4, s));
       t.valid[p] = false;
+      t.have_rs[p] = false;
     }
     t.vol = vol;
     t.w = rs->width;
@@ -2266,7 +2308,47 @@ static int tile_sched(vx_volume* vol, const vx_ray_setup* rs, int rank, int worl
 struct OrderJob {
   TileSched* ts = nullptr;
   int grid = 0;
+  int tiles_x = 0, rx = 0, ry = 0;  // camera motion in tiles (dilation radius)
 };
+
+// Image-space motion of the volume between two cameras, in tiles: the
+// largest displacement of the box corners and centre, per axis (capped at 4;
+// 4 when a point lies behind either camera).  Drives the cost dilation of
+// the tile order for a moving camera (0 for a static one).
+static void camera_motion_tiles(const vx_ray_setup* a, const vx_ray_setup* b, const vx_volume* v,
+                                int* rx, int* ry) {
+  *rx = *ry = 0;
+  if (!memcmp(a, b, sizeof(vx_ray_setup))) return;
+  const double lo = -0.5, hi[3] = {v->nx - 0.5, v->ny - 0.5, v->nz - 0.5};
+  double dxm = 0.0, dym = 0.0;
+  for (int k = 0; k < 9; ++k) {
+    double P[3];
+    for (int c = 0; c < 3; ++c)
+      P[c] = k == 8 ? 0.5 * (lo + hi[c]) : (((k >> c) & 1) ? hi[c] : lo);
+    double px[2], py[2];
+    const vx_ray_setup* cs[2] = {a, b};
+    for (int i = 0; i < 2; ++i) {
+      const vx_ray_setup* r = cs[i];
+      double q[3], z = 0.0, u = 0.0, w = 0.0;
+      for (int c = 0; c < 3; ++c) q[c] = P[c] - r->origin[c];
+      for (int c = 0; c < 3; ++c) {
+        z += q[c] * r->fwd[c];
+        u += q[c] * r->right[c];
+        w += q[c] * r->up[c];
+      }
+      if (z <= 1e-6) {
+        *rx = *ry = 4;
+        return;
+      }
+      px[i] = (u / z / (r->tan_f * r->aspect) + 1.0) * 0.5 * r->width;
+      py[i] = (1.0 - w / z / r->tan_f) * 0.5 * r->height;
+    }
+    dxm = fmax(dxm, fabs(px[1] - px[0]));
+    dym = fmax(dym, fabs(py[1] - py[0]));
+  }
+  *rx = (int)fmin(4.0, ceil(dxm / kTileW));
+  *ry = (int)fmin(4.0, ceil(dym / kTileH));
+}
 
 static int order_tiles(const OrderJob& j, cudaStream_t s) {
   if (!j.ts) return VX_OK;
@@ -2277,7 +2359,9 @@ static int order_tiles(const OrderJob& j, cudaStream_t s) {
   VX_CUDA(cudaStreamWaitEvent(ts->side, ts->costs_done[p], 0));
   tile_order_kernel<<<1, 1024, 0, ts->side>>>(b + j.grid + kSchedHdr, b, j.grid,
                                               g_sched_split_us.load(),
-                                              vx_sm_count() * (VX_RAYCAST_MIN_WARPS / kWarpsPerBlock));
+                                              vx_sm_count() * (VX_RAYCAST_MIN_WARPS / kWarpsPerBlock),
+                                              j.tiles_x, j.rx, j.ry,
+                                              b + 2 * j.grid + kSchedHdr);
   VX_CHECK_LAUNCH();
   // the split demand, read back without a sync: it sizes a later frame's
   // reserve of extra blocks (a stale value only costs time)
@@ -2417,6 +2501,16 @@ static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_p
   OrderJob job;
   job.ts = ts;
   job.grid = grid;
+  job.tiles_x = a.tiles_x;
+  if (ts && a.world == 1 && dilate_moving()) {
+    // the order this frame's costs produce serves frame k + 2: expect the
+    // camera to keep moving as it did from frame k - 2 (whose costs buf[p]
+    // held) to this frame
+    const int p = ts->parity;
+    if (ts->have_rs[p]) camera_motion_tiles(&ts->last_rs[p], rs, vol, &job.rx, &job.ry);
+    ts->last_rs[p] = *rs;
+    ts->have_rs[p] = true;
+  }
   if (defer) {
     *defer = job;
     return VX_OK;
