@@ -269,6 +269,34 @@ extern "C" int vx_group_connect(vx_group* g, const uint8_t* blobs, int32_t sync)
       g->ipc_open[r] = true;
     }
   }
+  if (sync == VX_GROUP_SYNC_DEVICE && g->world > 1) {
+    // probe the flag writes across the mapping (rank r > 0: its done slot in
+    // rank 0's block; rank 0: every peer's consumed flag) with the value the
+    // flags already hold (0), so a driver or topology that cannot do them
+    // fails here and the caller can fall back to VX_GROUP_SYNC_HOST
+    cudaStream_t ps;
+    VX_CUDA(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking));
+    int rc = VX_OK;
+    for (int r = 0; r < g->world && !rc; ++r) {
+      uint8_t* flag = nullptr;
+      if (g->rank > 0 && r == 0) flag = g->peer[0] + 4 * g->rank;
+      if (g->rank == 0 && r > 0) flag = g->peer[r] + kConsumedOff;
+      if (flag) rc = cu_check(g_write32((CUstream)ps, (CUdeviceptr)flag, 0u, 0), "peer flag probe");
+    }
+    cudaError_t e = cudaStreamSynchronize(ps);
+    cudaStreamDestroy(ps);
+    if (!rc && e != cudaSuccess) rc = vx_cuda_fail(e, "peer flag probe", __FILE__, __LINE__);
+    if (rc) {
+      for (int r = 0; r < g->world; ++r)
+        if (g->ipc_open[r]) {
+          cudaIpcCloseMemHandle(g->peer[r]);
+          g->ipc_open[r] = false;
+        }
+      for (int r = 0; r < g->world; ++r)
+        if (r != g->rank) g->peer[r] = nullptr;
+      return rc;
+    }
+  }
   g->sync = sync;
   g->connected = true;
   return VX_OK;

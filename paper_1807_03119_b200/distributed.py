@@ -159,16 +159,36 @@ class FrameGroup:
         self.world = dist.get_world_size(group)
         self.max_pixels = int(max_pixels)
         self.backend = backend if backend is not None else NativeGroup()
-        blob = self.backend.create(self.rank, self.world, self.max_pixels)
-        blobs = all_gather_bytes(blob, group)
         if sync == "auto":
             # decided collectively: every rank must agree on the protocol
             mode = (_lib.VX_GROUP_SYNC_HOST if self._shared(group) or not self._memops_ok(group)
                     else _lib.VX_GROUP_SYNC_DEVICE)
         else:
             mode = {"device": _lib.VX_GROUP_SYNC_DEVICE, "host": _lib.VX_GROUP_SYNC_HOST}[sync]
-        self.sync = self.backend.connect(b"".join(blobs), mode)
+        self.sync = self._setup(mode, group)
         self.frames = 0
+
+    def _setup(self, mode: int, group) -> int:
+        """create, all-gather the blobs, connect.  If the device flags fail
+        on any rank (connect probes them across the peer mappings), every
+        rank rebuilds its group with host ordering."""
+        import torch.distributed as dist
+
+        blob = self.backend.create(self.rank, self.world, self.max_pixels)
+        blobs = all_gather_bytes(blob, group)
+        try:
+            got, ok = self.backend.connect(b"".join(blobs), mode), True
+        except _lib.NativeError:
+            if mode != _lib.VX_GROUP_SYNC_DEVICE:
+                raise
+            got, ok = None, False
+        flags: list = [None] * self.world
+        dist.all_gather_object(flags, ok, group=group)
+        if all(flags):
+            return got
+        self.backend.close()
+        self.backend = type(self.backend)()
+        return self._setup(_lib.VX_GROUP_SYNC_HOST, group)
 
     def _memops_ok(self, group) -> bool:
         """Every rank's device supports the stream-memop flags."""

@@ -214,3 +214,63 @@ def test_gloo_frame_group_protocol(world, tmp_path):
         assert p.exitcode == 0
     assert all(ok for _, ok, _ in res)
     assert all(n == 4 for *_, n in res)
+
+
+class _FlakyGroup:
+    """Backend whose device-flag connect fails on rank 1 (e.g. no stream
+    memops across a peer mapping): every rank must end up host-ordered."""
+
+    def create(self, rank, world, max_pixels):
+        self.rank = rank
+        return b"x"
+
+    def shares_device(self, group):
+        return False
+
+    def probe_device_sync(self):
+        return True
+
+    def connect(self, blobs, sync):
+        from paper_1807_03119_b200 import _lib
+
+        if sync == _lib.VX_GROUP_SYNC_DEVICE and self.rank == 1:
+            raise _lib.NativeError(3, "peer flag probe failed (CUresult 801)")
+        return sync
+
+    def close(self):
+        pass
+
+
+def _fallback_worker(rank, world, port, q):
+    import sys
+
+    sys.path.insert(0, os.getcwd())
+    import torch.distributed as dist
+
+    from paper_1807_03119_b200 import _lib
+    from paper_1807_03119_b200.distributed import FrameGroup
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        fg = FrameGroup(100, backend=_FlakyGroup())
+        q.put((rank, fg.sync == _lib.VX_GROUP_SYNC_HOST, fg.host_sync))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_frame_group_falls_back_to_host_ordering():
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fallback_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(3)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(host and hs for _, host, hs in res)
