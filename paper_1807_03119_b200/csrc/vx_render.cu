@@ -612,6 +612,29 @@ __device__ __forceinline__ float sample_t(float base, float s, int k) {
   return __fadd_rn(base, __fmul_rn(s, (float)k));
 }
 
+// J steps of the chunk-base recurrence base <- fl(base + adv) in closed
+// form.  Every partial sum base + i*adv (0 < i <= J, all in [base, B]) is a
+// float -- so each rounding is exact and the sequential result is B = base
+// + J*adv -- when B is a float and base and adv are both multiples of
+// ulp(B): each partial sum is then a multiple of ulp(B) >= its own ulp.  B
+// itself is exact in FP64 (24-bit operands, J < 2^20).  Returns false when
+// the condition fails (the caller steps sequentially).
+#ifndef VX_CHUNK_JUMP
+#define VX_CHUNK_JUMP 1
+#endif
+__device__ __forceinline__ bool chunk_jump(float base, float adv, int J, float& out) {
+  const double B = __dadd_rn((double)base, __dmul_rn((double)J, (double)adv));
+  const float Bf = __double2float_rn(B);
+  if ((double)Bf != B || !(base >= 0.0f) || !(adv > 0.0f)) return false;
+  const unsigned e = (__float_as_uint(Bf) >> 23) & 0xffu;  // biased exponent of B
+  if (e < 24u || e > 253u) return false;
+  const float inv_u = __uint_as_float((277u - e) << 23);     // 2^(150 - e) = 1/ulp(B)
+  const float bs = __fmul_rn(base, inv_u), as = __fmul_rn(adv, inv_u);
+  if (bs != truncf(bs) || as != truncf(as)) return false;
+  out = Bf;
+  return true;
+}
+
 // first index in [lo, m] whose sample t exceeds lim (m if none); O(1):
 // estimate, then fix up against the exact sample t (monotone in k)
 __device__ __forceinline__ int first_beyond(float base, const MarchD& M, float lim, int lo, int m) {
@@ -789,6 +812,22 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
               // overhead per dependent add).  Measured per filter: local
               // cluster -1.5 % (bench frame) / -6.6 % (C4), the other kinds'
               // instantiations +2-5 % (register allocation), so LC only.
+              // whole chunks in closed form when every partial sum of the
+              // recurrence is exact (base_J = base + J*adv, see chunk_jump);
+              // otherwise (a skip crossing a binade with low bits set) the
+              // sequential recurrence below
+              if (VX_CHUNK_JUMP && g >= chunk && done < guard) {
+                const int jg = g / chunk;
+                const int jd = (guard - done + chunk - 1) / chunk;
+                const int J = jg < jd ? jg : jd;
+                float nb;
+                if (chunk_jump(base, M.adv, J, nb)) {
+                  VX_DIAG_ADD(dChunkLoop, J);
+                  base = nb;
+                  done += J * chunk;
+                  g -= J * chunk;
+                }
+              }
               if (KIND == VX_FILTER_LOCAL_CLUSTER || VX_CHUNK_UNROLL)
               while (g >= 4 * chunk && done + 3 * chunk < guard) {
                 VX_DIAG_ADD(dChunkLoop, 4);
