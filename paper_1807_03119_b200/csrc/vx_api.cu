@@ -262,7 +262,20 @@ int vx_volume_finish(vx_volume* v, const uint8_t* compact_dev, cudaStream_t s) {
     MapSlot* slot = nullptr;
     if (T > 0 && T <= 255) {
       if ((rc = vx_get_dist_map(v, T, &m, &slot, s))) return rc;
+      // and its eight orthant maps (~0.2 ms each at 1024^3): whatever the
+      // first camera, its frame finds its orthants built
+      unsigned built = 0;
+      {
+        std::lock_guard<std::mutex> lock(v->mu);
+        rc = vx_map_octants(v, slot, 0xffu, &built, s);
+      }
+      if (rc) return rc;
       if ((rc = vx_map_release(v, slot, s))) return rc;
+      // the first accepted-cell slot's occupancy and orthant blocks: a
+      // cudaMalloc inside a frame measured 1-97 ms
+      AccEntry& a0 = v->acc[0];
+      if (!a0.occ) VX_CUDA(cudaMalloc(&a0.occ, v->cmap_bytes));
+      if (!a0.oct) VX_CUDA(cudaMalloc(&a0.oct, 8 * v->cmap_bytes));
     }
     if ((rc = vx_preload_render_kernels())) return rc;
     // grow the stream-ordered pool once (it keeps freed memory: release
