@@ -473,14 +473,20 @@ __device__ __forceinline__ double filter_value(const VolView& V, const FiltD& F,
 // ---------------------------------------------------------------------------
 // ray setup (render.py:188-230)
 
-VX_COLD void ray_dir(const RayCamD& C, int i, int j, double d[3]) {
-  const double u = __dmul_rn(
+// u and v of pixel (i, j) (render.py:193-196)
+__device__ __forceinline__ double ray_u(const RayCamD& C, int i) {
+  return __dmul_rn(
       __dmul_rn(__dsub_rn(__ddiv_rn(__dmul_rn(2.0, __dadd_rn((double)i, 0.5)), (double)C.W), 1.0),
                 C.tan_f),
       C.aspect);
-  const double v =
-      __dmul_rn(__dsub_rn(1.0, __ddiv_rn(__dmul_rn(2.0, __dadd_rn((double)j, 0.5)), (double)C.H)),
-                C.tan_f);
+}
+__device__ __forceinline__ double ray_v(const RayCamD& C, int j) {
+  return __dmul_rn(__dsub_rn(1.0, __ddiv_rn(__dmul_rn(2.0, __dadd_rn((double)j, 0.5)), (double)C.H)),
+                   C.tan_f);
+}
+
+// the normalised direction from u, v (render.py:197-201)
+VX_COLD void ray_dir_uv(const RayCamD& C, double u, double v, double d[3]) {
 #pragma unroll
   for (int c = 0; c < 3; ++c)
     d[c] = __dadd_rn(__dadd_rn(C.fwd[c], __dmul_rn(u, C.right[c])), __dmul_rn(v, C.up[c]));
@@ -490,12 +496,8 @@ VX_COLD void ray_dir(const RayCamD& C, int i, int j, double d[3]) {
   for (int c = 0; c < 3; ++c) d[c] = __ddiv_rn(d[c], nrm);
 }
 
-// NaN-propagating min / max (np.minimum / np.maximum)
-__device__ __forceinline__ double nmin(double a, double b) {
-  return (a != a || b != b) ? __longlong_as_double(0x7ff8000000000000ll) : (a < b ? a : b);
-}
-__device__ __forceinline__ double nmax(double a, double b) {
-  return (a != a || b != b) ? __longlong_as_double(0x7ff8000000000000ll) : (a > b ? a : b);
+VX_COLD void ray_dir(const RayCamD& C, int i, int j, double d[3]) {
+  ray_dir_uv(C, ray_u(C, i), ray_v(C, j), d);
 }
 
 VX_COLD void ray_span(const double o[3], const double d[3], int nx, int ny,
@@ -504,6 +506,10 @@ VX_COLD void ray_span(const double o[3], const double d[3], int nx, int ny,
                         __dsub_rn((double)nz, 0.5)};
   double tmin = -__longlong_as_double(0x7ff0000000000000ll);
   double tmax = __longlong_as_double(0x7ff0000000000000ll);
+  // np.minimum / np.maximum propagate NaN: a NaN anywhere (0 * inf, only for
+  // a subnormal direction component) makes both results NaN, so it is
+  // tracked once instead of in every min / max
+  bool nan = false;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     double near, far;
@@ -516,13 +522,18 @@ VX_COLD void ray_span(const double o[3], const double d[3], int nx, int ny,
       const double inv = __ddiv_rn(1.0, d[a]);
       const double t1 = __dmul_rn(__dsub_rn(-0.5, o[a]), inv);
       const double t2 = __dmul_rn(__dsub_rn(hi[a], o[a]), inv);
-      near = nmin(t1, t2);
-      far = nmax(t1, t2);
+      nan = nan || t1 != t1 || t2 != t2;
+      near = t1 < t2 ? t1 : t2;
+      far = t1 > t2 ? t1 : t2;
     }
-    tmin = nmax(tmin, near);
-    tmax = nmin(tmax, far);
+    tmin = tmin > near ? tmin : near;
+    tmax = tmax < far ? tmax : far;
   }
-  t_enter = nmax(tmin, 0.0);
+  if (nan) {
+    t_enter = t_exit = __longlong_as_double(0x7ff8000000000000ll);
+    return;
+  }
+  t_enter = tmin > 0.0 ? tmin : 0.0;
   t_exit = tmax;
 }
 
@@ -1284,14 +1295,21 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     block_t0 = t;
   }
-  if (KIND == VX_FILTER_ENTROPY || a.tile_cost) __syncthreads();
+  const int tile = a.rank + a.world * owned;
+  const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+  // the tile's 8 column u and 16 row v (one FP64 division each, render.py:
+  // 193-196) once per block instead of per pixel
+  __shared__ double su[kTileW], sv[kTileH];
+  if (tid < kTileW)
+    su[tid] = ray_u(a.C, tx * kTileW + tid);
+  else if (tid < kTileW + kTileH)
+    sv[tid - kTileW] = ray_v(a.C, ty * kTileH + (tid - kTileW));
+  __syncthreads();
 
 #ifdef VX_WARP_TIMING
   unsigned long long wt0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(wt0));
 #endif
-  const int tile = a.rank + a.world * owned;
-  const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int rpw = 32 / nseg;  // rays per warp
   const int seg = (int)(tid & 31) / rpw;
   const int ray = (int)(tid & 31) % rpw;
@@ -1318,7 +1336,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
   double hval = 0.0;
   if (valid) {
     double d[3];
-    ray_dir(a.C, i, j, d);
+    ray_dir_uv(a.C, su[i - tx * kTileW], sv[j - ty * kTileH], d);
     double te, tx_;
     ray_span(a.C.origin, d, a.V.nx, a.V.ny, a.V.nz, te, tx_);
     hx = hy = hz = -1;
@@ -1402,7 +1420,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
       // the FP64 direction is recomputed (bit-identical) instead of being
       // kept live in registers across the march
       double d[3];
-      ray_dir(a.C, i, j, d);
+      ray_dir_uv(a.C, su[i - tx * kTileW], sv[j - ty * kTileH], d);
       const double view[3] = {-d[0], -d[1], -d[2]};
       double n[3];
       sobel<CHECKED>(a.V, hx, hy, hz, view, n);
