@@ -302,14 +302,6 @@ extern "C" int vx_group_connect(vx_group* g, const uint8_t* blobs, int32_t sync)
   return VX_OK;
 }
 
-// stream-ordered wait until the 32-bit word at addr reaches value (cyclic >=)
-int vx_stream_wait_geq(cudaStream_t s, const void* addr, uint32_t value) {
-  int rc = load_memops();
-  if (rc) return rc;
-  return cu_check(g_wait32((CUstream)s, (CUdeviceptr)addr, value, CU_STREAM_WAIT_VALUE_GEQ),
-                  "cuStreamWaitValue32");
-}
-
 extern "C" int vx_group_probe_device_sync(void) {
   int rc = load_memops();
   if (rc) return rc;

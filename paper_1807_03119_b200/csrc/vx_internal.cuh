@@ -249,9 +249,6 @@ int vx_launch_phantom(uint8_t* dst, int64_t row_pitch, int64_t plane_pitch, int6
                       double noise_sigma, uint64_t noise_seed, const int64_t* spot_idx,
                       int64_t n_spots, int32_t spot_intensity, cudaStream_t s);
 int vx_preload_render_kernels();
-// stream-ordered wait until the u32 at addr reaches value (cyclic >=;
-// cuStreamWaitValue32, vx_group.cu)
-int vx_stream_wait_geq(cudaStream_t s, const void* addr, uint32_t value);
 // K4 into device outputs that may live in another rank's memory (peer /
 // IPC-mapped): sys_atomics selects system-scope counter atomics
 int vx_render_tiles(vx_volume* vol, const vx_ray_setup* rs, const vx_render_params* rp,

@@ -35,7 +35,6 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <thread>
 
 #include "vx_internal.cuh"
 
@@ -144,10 +143,6 @@ struct OutD {
   int32_t* trunc_flag;
   // outputs live in another rank's memory (vx_group): system-scope atomics
   int sys;
-  // band copy (vx_render): running count of pixels written per band of
-  // 2^band_shift rows, awaited by the band's copy stream (nullable)
-  unsigned* band_px;
-  int band_shift;
 };
 
 // counter update of K4's fused outputs (device scope, or system scope when
@@ -1499,18 +1494,6 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
     if (valid && (__ffs(peers) - 1) == (int)lane)
       out_add(a.O.image_hist + pix_out, (unsigned long long)__popc(peers), a.O.sys);
   }
-  if (a.O.band_px) {
-    // this warp's pixels (all in one band: bands are >= 16 rows, tile
-    // aligned) are in place: add them to the band's running count, which the
-    // band's copy stream awaits -- the frame goes back to the host band by
-    // band while the rest of the frame is still rendering
-    const unsigned wrote = __ballot_sync(0xffffffffu, valid);
-    __syncwarp();
-    if (lane == 0 && wrote) {
-      __threadfence();
-      atomicAdd(a.O.band_px + (j >> a.O.band_shift), (unsigned)__popc(wrote));
-    }
-  }
 }
 
 // frame-wide longest span (render.py:469-473), exact fallback budget
@@ -2073,17 +2056,6 @@ static double trace_us() {
     }                                                                             \
   } while (0)
 
-// band copy of vx_render's host frames; VOXB200_BAND_COPY=0 copies the
-// whole frame after the kernel
-constexpr int kMaxBands = 16;
-static bool band_copy_on() {
-  static const bool on = [] {
-    const char* e = getenv("VOXB200_BAND_COPY");
-    return !e || atoi(e) != 0;
-  }();
-  return on;
-}
-
 // Cost dilation of the tile order for a moving camera (VOXB200_DILATE=1).
 // Measured (scripts/orbit_probe.py, 1 degree per frame): device p50 0.194
 // ms dilated vs 0.159 ms on the plain k-2 costs -- the max filter turns the
@@ -2465,8 +2437,7 @@ static int order_tiles(const OrderJob& j, cudaStream_t s) {
 static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_params* rp,
                        const vx_filter_config* fc, const vx_partition* part, vx_render_out* o,
                        cudaStream_t s, int explicit_budget_override, OrderJob* defer = nullptr,
-                       bool sys_atomics = false, unsigned* band_px = nullptr,
-                       int band_shift = 0) {
+                       bool sys_atomics = false) {
   if (!vol || !rs || !rp || !fc || !o || !o->pixels) {
     vx_set_error("vx_render: null argument");
     return VX_EINVAL;
@@ -2540,8 +2511,6 @@ static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_p
   a.O.diag = reinterpret_cast<unsigned long long*>(o->diag);
   a.O.trunc_flag = o->trunc_flag;
   a.O.sys = sys_atomics ? 1 : 0;
-  a.O.band_px = band_px;
-  a.O.band_shift = band_shift;
   a.world = part ? part->world : 1;
   a.rank = part ? part->rank : 0;
   if (a.world < 1 || a.rank < 0 || a.rank >= a.world) {
@@ -2738,14 +2707,6 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
   static thread_local struct Staging {
     uint8_t* p = nullptr;
     size_t cap = 0;
-    // band copy: running per-band pixel counts (64 u32), frames counted
-    // into them, the frame size they count, the band streams and events
-    unsigned* bands = nullptr;
-    uint32_t frames = 0;
-    int bw = 0, bh = 0;
-    cudaStream_t cs[kMaxBands] = {};
-    cudaEvent_t cev[kMaxBands] = {};
-    cudaEvent_t start = nullptr;
   } staging[64];
   {
     int dev = 0;
@@ -2764,37 +2725,6 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
   uint8_t* base = st.p;
   VX_CUDA(cudaMemsetAsync(base + o_small, 0, 256 * 8 + 3 * 8 + 8 + 64, s));
   if (part && part->world > 1) VX_CUDA(cudaMemsetAsync(base + o_pix, 0, npx, s));
-  // Band copy: ~8 bands of 2^k >= 16 rows, each copied back on its own
-  // stream as soon as K4 has written all of its pixels (cuStreamWaitValue32
-  // on the band's running pixel count), instead of the whole frame after
-  // the kernel: only the last band's copy stays behind the kernel's end.
-  int band_rows = 16, band_shift = 4;
-  while (band_rows * 8 < rs->height && band_rows < (1 << 20)) {
-    band_rows <<= 1;
-    ++band_shift;
-  }
-  const int nbands = (rs->height + band_rows - 1) / band_rows;
-  const bool bands = band_copy_on() && !(part && part->world > 1) && npx >= 65536 &&
-                     nbands >= 2 && nbands <= kMaxBands;
-  if (bands) {
-    if (!st.bands) {
-      VX_CUDA(cudaMalloc(&st.bands, kMaxBands * 4));
-      VX_CUDA(cudaMemset(st.bands, 0, kMaxBands * 4));
-      VX_CUDA(cudaEventCreateWithFlags(&st.start, cudaEventDisableTiming));
-      for (int b = 0; b < kMaxBands; ++b) {
-        VX_CUDA(cudaStreamCreateWithFlags(&st.cs[b], cudaStreamNonBlocking));
-        VX_CUDA(cudaEventCreateWithFlags(&st.cev[b], cudaEventDisableTiming));
-      }
-    }
-    if (st.bw != rs->width || st.bh != rs->height) {  // counts restart with the frame size
-      VX_CUDA(cudaMemsetAsync(st.bands, 0, kMaxBands * 4, s));
-      st.frames = 0;
-      st.bw = rs->width;
-      st.bh = rs->height;
-    }
-    // the band streams start after everything queued so far (the reset)
-    VX_CUDA(cudaEventRecord(st.start, s));
-  }
   VX_TRACE("staging", tv);
   vx_render_out d;
   d.pixels = base + o_pix;
@@ -2817,8 +2747,7 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
     VX_CUDA(cudaEventRecord(ev[0], s));
   }
   OrderJob order;
-  rc = render_impl(vol, rs, rp, fc, part, &d, s, 0, &order, false, bands ? st.bands : nullptr,
-                   band_shift);
+  rc = render_impl(vol, rs, rp, fc, part, &d, s, 0, &order);
   if (rc) return rc;
   if (timed) VX_CUDA(cudaEventRecord(ev[1], s));
   float ms = 0.0f;
@@ -2829,50 +2758,8 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
   uint64_t small_h[267];
   cudaEvent_t copied = nullptr;
   VX_CUDA(copy_event(&copied));
-  uint32_t expect[kMaxBands] = {};
-  // waits for an event, polling; a band copy whose count never arrives (a
-  // bug) is released after 20 s instead of hanging the caller and the GPU
-  auto wait_event = [&](cudaEvent_t e) -> int {
-    const auto t0 = std::chrono::steady_clock::now();
-    for (;;) {
-      const cudaError_t q = cudaEventQuery(e);
-      if (q == cudaSuccess) return VX_OK;
-      if (q != cudaErrorNotReady) return vx_cuda_fail(q, "cudaEventQuery", __FILE__, __LINE__);
-      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20)) {
-        cudaStream_t rel;
-        cudaStreamCreateWithFlags(&rel, cudaStreamNonBlocking);
-        // the awaited counts themselves satisfy the waits
-        cudaMemcpyAsync(st.bands, expect, sizeof(expect), cudaMemcpyHostToDevice, rel);
-        cudaStreamSynchronize(rel);
-        cudaStreamDestroy(rel);
-        vx_set_error("vx_render: band copy timed out (pixel counts never arrived)");
-        return VX_ECUDA;
-      }
-      std::this_thread::yield();
-    }
-  };
   auto copy_back = [&]() -> int {
-    if (bands) {
-      const uint32_t k = ++st.frames;
-      for (int b = 0; b < nbands; ++b) {
-        const int r0 = b * band_rows;
-        const int rows = rs->height - r0 < band_rows ? rs->height - r0 : band_rows;
-        const size_t bytes = (size_t)rows * rs->width;
-        VX_CUDA(cudaStreamWaitEvent(st.cs[b], st.start, 0));
-        expect[b] = k * (uint32_t)bytes;
-        int r3 = vx_stream_wait_geq(st.cs[b], st.bands + b, expect[b]);
-        if (r3) return r3;
-        VX_CUDA(cudaMemcpyAsync(out->pixels + (size_t)r0 * rs->width,
-                                d.pixels + (size_t)r0 * rs->width, bytes,
-                                cudaMemcpyDeviceToHost, st.cs[b]));
-        VX_CUDA(cudaEventRecord(st.cev[b], st.cs[b]));
-      }
-      if (fused)  // histogram, hit count, samples, flag (behind the pixels)
-        VX_CUDA(cudaMemcpyAsync(out->pixels + o_fused, base + o_fused, 259 * 8,
-                                cudaMemcpyDeviceToHost, s));
-      else
-        VX_CUDA(cudaMemcpyAsync(small_h, small, sizeof(small_h), cudaMemcpyDeviceToHost, s));
-    } else if (fused) {  // pixels, padding, histogram, hit count, samples, flag
+    if (fused) {  // pixels, padding, histogram, hit count, samples, flag
       VX_CUDA(cudaMemcpyAsync(out->pixels, d.pixels, o_fused + 259 * 8, cudaMemcpyDeviceToHost, s));
     } else {
       VX_CUDA(cudaMemcpyAsync(out->pixels, d.pixels, npx, cudaMemcpyDeviceToHost, s));
@@ -2889,10 +2776,6 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
     int r2 = order_tiles(order, s);
     order = OrderJob();
     if (r2) return r2;
-    if (bands) {
-      for (int b = 0; b < nbands; ++b)
-        if ((r2 = wait_event(st.cev[b]))) return r2;
-    }
     VX_CUDA(cudaEventSynchronize(copied));
     if (fused) memcpy(small_h, out->image_hist, 259 * 8);
     return VX_OK;
@@ -2911,9 +2794,7 @@ extern "C" int vx_render(vx_volume* vol, const vx_ray_setup* rs, const vx_render
     if (rc) return rc;
     VX_CUDA(cudaMemsetAsync(small, 0, 267 * 8, s));
     if (timed) VX_CUDA(cudaEventRecord(ev[0], s));
-    if (bands) VX_CUDA(cudaEventRecord(st.start, s));
-    rc = render_impl(vol, rs, rp, fc, part, &d, s, budget, &order, false,
-                     bands ? st.bands : nullptr, band_shift);
+    rc = render_impl(vol, rs, rp, fc, part, &d, s, budget, &order);
     if (rc) return rc;
     if (timed) VX_CUDA(cudaEventRecord(ev[1], s));
     rc = copy_back();
