@@ -1843,32 +1843,9 @@ ShadeD make_shade(const vx_render_params* rp) {
   return S;
 }
 
-// K4's L1 / shared split: VX_K4_CARVEOUT = preferred shared-memory carveout
-// in percent (0: the largest L1); < 0 leaves the driver's choice
-#ifndef VX_K4_CARVEOUT
-#define VX_K4_CARVEOUT -1
-#endif
-template <typename Kern>
-static void k4_carveout(Kern kern) {
-  if (VX_K4_CARVEOUT < 0) return;
-  static std::atomic<unsigned long long> done{0};  // per instantiation, per device
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const unsigned long long bit = 1ull << (dev & 63);
-  if (done.load() & bit) return;
-  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, VX_K4_CARVEOUT);
-  cudaGetLastError();
-  done.fetch_or(bit);
-}
-
 template <int KIND, bool CHECKED>
 void launch_raycast(const RenderArgs& a, int grid, cudaStream_t s) {
   const dim3 blk(kTileW, 4 * kWarpsPerBlock);
-  k4_carveout(raycast_kernel<KIND, CHECKED, false, true>);
-  k4_carveout(raycast_kernel<KIND, CHECKED, true, true>);
-  k4_carveout(raycast_kernel<KIND, CHECKED, true, false>);
-  k4_carveout(raycast_kernel<KIND, CHECKED, false, false, false>);
-  k4_carveout(raycast_kernel<KIND, CHECKED, false, false>);
   grid *= kBlocksPerTile;
   // unbudgeted launches reserve split_max extra blocks for split tiles
   const int grid_u = grid + (kSplitRays && a.tile_order ? a.split_max : 0);
