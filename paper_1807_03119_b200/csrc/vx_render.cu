@@ -631,7 +631,7 @@ __device__ __forceinline__ float sample_t(float base, float s, int k) {
 // itself is exact in FP64 (24-bit operands, J < 2^20).  Returns false when
 // the condition fails (the caller steps sequentially).
 #ifndef VX_CHUNK_JUMP
-#define VX_CHUNK_JUMP 0  // measured slower (profiles/r2/r2_ab_chunk_jump.txt): off
+#define VX_CHUNK_JUMP 0  // measured slower (profiles/r2/r2_ab_misc.txt): off
 #endif
 __device__ __forceinline__ bool chunk_jump(float base, float adv, int J, float& out) {
   const double B = __dadd_rn((double)base, __dmul_rn((double)J, (double)adv));
