@@ -155,7 +155,11 @@ extern "C" int vx_group_create(int32_t rank, int32_t world, int64_t max_pixels, 
   g->world = world;
   g->max_pixels = max_pixels;
   g->slot_bytes = (slot_pixels(max_pixels) + kCounters * 8 + 255) & ~uint64_t(255);
-  VX_CUDA(cudaGetDevice(&g->device));
+  cudaError_t e0 = cudaGetDevice(&g->device);
+  if (e0 != cudaSuccess) {
+    delete g;
+    return vx_cuda_fail(e0, "cudaGetDevice", __FILE__, __LINE__);
+  }
   g->local_bytes = kFlagBytes + (rank == 0 ? 2 * g->slot_bytes : 0);
   cudaError_t e = cudaMalloc(&g->local, g->local_bytes);
   if (e != cudaSuccess) {

@@ -67,3 +67,7 @@ for w in top:
           f"part {part[w]} sm {sm[w]} | " + " ".join(f"{k}={int(x)}" for k, x in zip(names, dg[w])))
 med = np.median(dg, axis=0)
 print("  median warp: " + " ".join(f"{k}={x:.0f}" for k, x in zip(names, med)))
+# occupancy over time: resident warps per 5% of the span
+edges = np.linspace(0, e.max(), 21)
+occ = [int(((s < b) & (e > a)).sum()) for a, b in zip(edges[:-1], edges[1:])]
+print("warps alive per 5% of the span:", occ)
