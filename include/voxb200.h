@@ -281,6 +281,26 @@ int vx_group_download(vx_group* g, uint8_t* host_pixels, uint64_t* host_counters
                       int64_t n_pixels, void* stream);
 int vx_group_destroy(vx_group* g);
 
+/* ---- one process, several GPUs (SURVEY.md §8b vx_init) -------------------
+ * vx_init selects the devices (device_ids[0] renders the frame's owner
+ * slot).  vx_multi_volume_create_u8 builds a replica on every listed device
+ * (host upload to the first, device-to-device copies to the others);
+ * vx_multi_render renders one frame split over them (the frame group of
+ * vx_group_*, ranks = the listed devices, peer stores into the first
+ * device's frame, device flags when the devices are distinct) and returns the
+ * host frame like vx_render; vx_multi_histogram sums z-slab histograms of the
+ * replicas.  The same device may be listed twice (functional tests on one
+ * GPU: the frames are then ordered on the host). */
+typedef struct vx_multi vx_multi;
+int vx_init(int n_devices, const int* device_ids);
+int vx_multi_volume_create_u8(const uint8_t* host, int64_t nx, int64_t ny, int64_t nz,
+                              vx_multi** out);
+int vx_multi_render(vx_multi* m, const vx_ray_setup* rs, const vx_render_params* rp,
+                    const vx_filter_config* fc, vx_render_out* host_out);
+int vx_multi_histogram(vx_multi* m, uint64_t counts_out[256]);
+int vx_multi_info(const vx_multi* m, int32_t* n_devices_out, int32_t* sync_out);
+int vx_multi_destroy(vx_multi* m);
+
 /* ---- phantom input generator (volume.py:317-368; inputs only) ------------ */
 /* shape kinds: 0 sphere, 1 shell, 2 box; params per shape:
  * [kind, cx, cy, cz, intensity, radius, thickness, ex, ey, ez] as doubles.

@@ -18,7 +18,7 @@ LIB = PKG / "libvoxb200.so"
 CHECKED_LIB = PKG / "libvoxb200_checked.so"
 INCLUDE = PKG.parent / "include"
 
-SOURCES = ["vx_api.cu", "vx_hist.cu", "vx_volume.cu", "vx_render.cu", "vx_io.cu", "vx_group.cu"]
+SOURCES = ["vx_api.cu", "vx_hist.cu", "vx_volume.cu", "vx_render.cu", "vx_io.cu", "vx_group.cu", "vx_multi.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

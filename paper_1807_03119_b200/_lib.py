@@ -169,6 +169,12 @@ SIGNATURES = {
     "vx_group_release": [P, P],
     "vx_group_download": [P, P, P, I64, P],
     "vx_group_destroy": [P],
+    "vx_init": [C.c_int, P],
+    "vx_multi_volume_create_u8": [P, I64, I64, I64, P],
+    "vx_multi_render": [P, P, P, P, P],
+    "vx_multi_histogram": [P, P],
+    "vx_multi_info": [P, P, P],
+    "vx_multi_destroy": [P],
 }
 _RESTYPES = {"vx_last_error": C.c_char_p}
 

@@ -2262,7 +2262,14 @@ struct TileSched {
   vx_ray_setup last_rs[2];  // camera of the frame that recorded costs into buf[p]
   bool have_rs[2] = {false, false};
 };
-static thread_local TileSched tl_sched;
+// a thread's schedules, one per (volume, frame size, partition, stream):
+// a thread alternating between frames of several kinds -- or enqueueing
+// every device's tiles of a multi-device frame (vx_multi.cu) -- keeps each
+// schedule instead of rebuilding one (LRU of 8)
+constexpr int kSchedSlots = 8;
+static thread_local TileSched tl_sched[kSchedSlots];
+static thread_local uint64_t tl_sched_use[kSchedSlots];
+static thread_local uint64_t tl_sched_clock = 0;
 
 // scheduling knobs (vx_set_schedule): order on/off, smallest grid (in tiles,
 // -1 = 4 waves of SMs) that gets an order, split threshold (us), split cap
@@ -2316,13 +2323,38 @@ static int tile_sched(vx_volume* vol, const vx_ray_setup* rs, int rank, int worl
   // small frames fit in one wave of blocks: nothing to reorder
   const int min_grid = g_sched_min_grid.load() < 0 ? 4 * vx_sm_count() : g_sched_min_grid.load();
   if (!enabled || grid < min_grid) return VX_OK;
-  TileSched& t = tl_sched;
+  int cur_dev = 0;
+  VX_CUDA(cudaGetDevice(&cur_dev));
+  int pick = -1;
+  for (int i = 0; i < kSchedSlots && pick < 0; ++i) {
+    const TileSched& c = tl_sched[i];
+    if (c.vol == vol && c.w == rs->width && c.h == rs->height && c.rank == rank &&
+        c.world == world && c.grid == grid && c.stream == s && c.device == cur_dev && c.buf[0])
+      pick = i;
+  }
+  if (pick < 0) {  // least recently used slot (an empty one first)
+    pick = 0;
+    for (int i = 1; i < kSchedSlots; ++i)
+      if (tl_sched_use[i] < tl_sched_use[pick]) pick = i;
+  }
+  tl_sched_use[pick] = ++tl_sched_clock;
+  TileSched& t = tl_sched[pick];
   int dev = 0;
   VX_CUDA(cudaGetDevice(&dev));
   if (t.device != dev) {  // per-thread side stream and events of this device
-    if (t.side) {
+    if (t.side) {  // the slot served another device: release its resources there
+      VX_CUDA(cudaSetDevice(t.device));
       VX_CUDA(cudaStreamSynchronize(t.side));
-      t.vol = nullptr;  // buffers belong to the old device: rebuild below
+      if (t.stream) VX_CUDA(cudaStreamSynchronize(t.stream));
+      for (int p = 0; p < 2; ++p) {
+        if (t.buf[p]) VX_CUDA(cudaFree(t.buf[p]));
+        VX_CUDA(cudaEventDestroy(t.costs_done[p]));
+        VX_CUDA(cudaEventDestroy(t.order_done[p]));
+        t.valid[p] = false;
+      }
+      VX_CUDA(cudaStreamDestroy(t.side));
+      VX_CUDA(cudaSetDevice(dev));
+      t.vol = nullptr;  // rebuilt below
     }
     VX_CUDA(cudaStreamCreateWithFlags(&t.side, cudaStreamNonBlocking));
     for (int p = 0; p < 2; ++p) {

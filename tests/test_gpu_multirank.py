@@ -199,3 +199,47 @@ def test_group_device_flags_two_threads(vx, small_sphere_volume, small_sphere_hi
         _lib.call("vx_synchronize")
         for g in gs:
             lib.vx_group_destroy(g)
+
+
+def test_vx_init_multi_device_frames(vx, small_sphere_volume, small_sphere_histogram):
+    """SURVEY §8b's vx_init + the multi-device volume/frame: the listed
+    devices each hold a replica, a frame is split over them (here device 0
+    listed three times: host-ordered, the same peer-slot data path) and
+    equals the single-device frame; the slab-sharded histogram equals K1."""
+    from paper_1807_03119_b200 import _lib
+    from paper_1807_03119_b200.filters import native_config
+    from paper_1807_03119_b200.render import native_params, ray_setup
+
+    lib = _lib.load()
+    ids = (C.c_int * 3)(0, 0, 0)
+    _lib.call("vx_init", 3, ids)
+    m = C.c_void_p()
+    data = np.ascontiguousarray(small_sphere_volume.data)
+    _lib.call("vx_multi_volume_create_u8", _lib.ptr(data), *small_sphere_volume.dims, C.byref(m))
+    try:
+        n, sync = C.c_int32(), C.c_int32()
+        _lib.call("vx_multi_info", m, C.byref(n), C.byref(sync))
+        assert n.value == 3 and sync.value == _lib.VX_GROUP_SYNC_HOST
+        counts = np.zeros(256, np.uint64)
+        _lib.call("vx_multi_histogram", m, _lib.ptr(counts))
+        assert np.array_equal(counts.astype(np.int64), small_sphere_histogram.counts)
+        for W, H, az in ((96, 72, 30.0), (130, 50, 200.0), (96, 72, 75.0)):
+            cam = vx.orbit_camera(small_sphere_volume, azimuth_deg=az)
+            params = vx.RenderParams(width=W, height=H)
+            cfg = vx.FilterConfig(kind=vx.FilterKind.SIGMA).resolve_threshold(small_sphere_histogram)
+            want = vx.render_frame(small_sphere_volume, cam, params, cfg, small_sphere_histogram)
+            rs, rp = ray_setup(cam, W, H), native_params(params)
+            fc = native_config(cfg, small_sphere_histogram)
+            pix = np.zeros((H, W), np.uint8)
+            hist = np.zeros(256, np.uint64)
+            hits = np.zeros(1, np.uint64)
+            out = _lib.vx_render_out()
+            out.pixels, out.image_hist, out.hit_count = pix.ctypes.data, hist.ctypes.data, hits.ctypes.data
+            _lib.call("vx_multi_render", m, C.byref(rs), C.byref(rp), C.byref(fc), C.byref(out))
+            assert np.array_equal(pix, want.pixels), (W, H, az)
+            assert int(hits[0]) == want.hit_count
+            assert np.array_equal(hist.astype(np.int64),
+                                  np.bincount(want.pixels.reshape(-1), minlength=256))
+    finally:
+        lib.vx_multi_destroy(m)
+        _lib.call("vx_init", 1, (C.c_int * 1)(0))
