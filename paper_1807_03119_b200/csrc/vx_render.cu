@@ -677,7 +677,10 @@ __device__ __forceinline__ int first_beyond(float base, const MarchD& M, float l
 // wl: this warp's 32-int shared scratch.  All 32 lanes must call.
 // limit = the lane's sample budget.  Returns kHit, kMiss (left the span or
 // inactive) or kExhausted (budget ran out while still inside the span).
-template <int KIND, bool CHECKED, bool DIAG, bool BUDGET, bool SKIP = true>
+// RAY_ORIGIN: rays have their own origins (march_ray); false: one camera
+// origin for every ray of the frame, so the lanes that load or evaluate for
+// another lane's ray use their own copy instead of shuffling it
+template <int KIND, bool CHECKED, bool DIAG, bool BUDGET, bool SKIP = true, bool RAY_ORIGIN = false>
 __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const double* lut,
                      const RayState& R, bool active, int limit, int done0, int stop,
                      float& ht, int& hidx, unsigned& nsamp, Diag& dg, WarpScratch* ws) {
@@ -915,9 +918,9 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
         const int sk = __shfl_sync(0xffffffffu, k, src);
         const int sm = __shfl_sync(0xffffffffu, m, src);
         const float st = __shfl_sync(0xffffffffu, tend, src);
-        const float o0 = __shfl_sync(0xffffffffu, R.o[0], src);
-        const float o1 = __shfl_sync(0xffffffffu, R.o[1], src);
-        const float o2 = __shfl_sync(0xffffffffu, R.o[2], src);
+        const float o0 = RAY_ORIGIN ? __shfl_sync(0xffffffffu, R.o[0], src) : R.o[0];
+        const float o1 = RAY_ORIGIN ? __shfl_sync(0xffffffffu, R.o[1], src) : R.o[1];
+        const float o2 = RAY_ORIGIN ? __shfl_sync(0xffffffffu, R.o[2], src) : R.o[2];
         const float d0 = __shfl_sync(0xffffffffu, R.d[0], src);
         const float d1 = __shfl_sync(0xffffffffu, R.d[1], src);
         const float d2 = __shfl_sync(0xffffffffu, R.d[2], src);
@@ -1124,9 +1127,9 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
           const int owner = item >> 3, j = item & 7;
           const float ob = __shfl_sync(0xffffffffu, base, owner);
           const int okk = __shfl_sync(0xffffffffu, k, owner);
-          const float o0 = __shfl_sync(0xffffffffu, R.o[0], owner);
-          const float o1 = __shfl_sync(0xffffffffu, R.o[1], owner);
-          const float o2 = __shfl_sync(0xffffffffu, R.o[2], owner);
+          const float o0 = RAY_ORIGIN ? __shfl_sync(0xffffffffu, R.o[0], owner) : R.o[0];
+          const float o1 = RAY_ORIGIN ? __shfl_sync(0xffffffffu, R.o[1], owner) : R.o[1];
+          const float o2 = RAY_ORIGIN ? __shfl_sync(0xffffffffu, R.o[2], owner) : R.o[2];
           const float d0 = __shfl_sync(0xffffffffu, R.d[0], owner);
           const float d1 = __shfl_sync(0xffffffffu, R.d[1], owner);
           const float d2 = __shfl_sync(0xffffffffu, R.d[2], owner);
@@ -1334,6 +1337,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
   int hx = -1, hy = -1, hz = -1, hidx = 0;
   float ht = 0.0f;
   double hval = 0.0;
+  // the frame's one origin, on every lane (march reads it for other lanes' rays)
+#pragma unroll
+  for (int c = 0; c < 3; ++c) R.o[c] = __double2float_rn(__dadd_rn(a.C.origin[c], 0.5));
   if (valid) {
     double d[3];
     ray_dir_uv(a.C, su[i - tx * kTileW], sv[j - ty * kTileH], d);
@@ -1343,10 +1349,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
     live = tx_ >= te && a.M.thr <= 255;
     if (live) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        R.o[c] = __double2float_rn(__dadd_rn(a.C.origin[c], 0.5));
-        R.d[c] = __double2float_rn(d[c]);
-      }
+      for (int c = 0; c < 3; ++c) R.d[c] = __double2float_rn(d[c]);
       ray_skip_consts(R);
       ray_skip_map(R, a.V);
       R.base = __double2float_rn(te);
@@ -1672,7 +1675,7 @@ __global__ void march_rays_kernel(VolView V, MarchD M, FiltD F, const double* __
     }
   }
   Diag dg;
-  const bool hit = march<KIND, CHECKED, false, true>(V, M, F, lut_g, R, live, limit, 0, 0, ht,
+  const bool hit = march<KIND, CHECKED, false, true, true, true>(V, M, F, lut_g, R, live, limit, 0, 0, ht,
                                                      hidx, nsamp, dg, &wsc[threadIdx.x >> 5]) == kHit;
   if (hit) {
     voxel_at(R, M, ht, hx, hy, hz);
