@@ -916,7 +916,8 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
         const int src = wl[q < nr ? q : 0];  // spare slots repeat a real ray: loads stay legal
         const float sb = __shfl_sync(0xffffffffu, base, src);
         const int sk = __shfl_sync(0xffffffffu, k, src);
-        const int sm = __shfl_sync(0xffffffffu, m, src);
+        // unbudgeted chunks are always full: m == chunk on every lane
+        const int sm = BUDGET ? __shfl_sync(0xffffffffu, m, src) : chunk;
         const float st = __shfl_sync(0xffffffffu, tend, src);
         const float o0 = RAY_ORIGIN ? __shfl_sync(0xffffffffu, R.o[0], src) : R.o[0];
         const float o1 = RAY_ORIGIN ? __shfl_sync(0xffffffffu, R.o[1], src) : R.o[1];
