@@ -18,8 +18,10 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import threading
 import time
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -492,11 +494,22 @@ class frame_timing:
 
 def render_frame(volume: Volume, camera: Camera, params: RenderParams, config: FilterConfig,
                  histogram: HistogramModel | None = None, workers: int = 1,
-                 filter_fn=None) -> Frame:
-    """Render one frame on the B200; bit-identical output for any worker count."""
+                 filter_fn=None, devices=None) -> Frame:
+    """Render one frame on the B200; bit-identical output for any worker count.
+
+    ``devices`` (or env VOXB200_DEVICES="0,1,..."): split the frame over
+    these GPUs from this process (vx_init + vx_multi_render,
+    a replica per device, tiles dealt round-robin, peer stores into the first
+    device's frame).  The pixels do not depend on it, as they do not depend
+    on ``workers`` (render.py:514-541).
+    """
     wall0 = time.perf_counter()
     config = _check_render_args(config, histogram, filter_fn)
-    d = render_detail(volume, camera, params, config, histogram, _checked=True)
+    devs = _devices(devices)
+    if devs is not None and len(devs) > 1:
+        d = _render_multi(volume, camera, params, config, histogram, devs)
+    else:
+        d = render_detail(volume, camera, params, config, histogram, _checked=True)
     total_ms = (time.perf_counter() - wall0) * 1000.0
     frame = Frame(
         pixels=d.pixels,
@@ -514,3 +527,76 @@ def render_frame(volume: Volume, camera: Camera, params: RenderParams, config: F
     )
     frame.image_hist = d.image_hist
     return frame
+
+
+# --- one process, several GPUs (vx_init / vx_multi_*) ----------------------------------
+
+
+def _devices(devices):
+    if devices is None:
+        env = os.environ.get("VOXB200_DEVICES")
+        if not env:
+            return None
+        devices = [int(v) for v in env.split(",") if v.strip()]
+    return tuple(int(v) for v in devices)
+
+
+class MultiVolume:
+    """Owning handle of a vx_multi (a replica on each listed device)."""
+
+    def __init__(self, volume: Volume, devices: tuple):
+        _lib.require_device()
+        ids = (C.c_int * len(devices))(*devices)
+        _lib.call("vx_init", len(devices), ids, exc_type=RenderError)
+        self.handle = C.c_void_p()
+        data = np.ascontiguousarray(volume.data)
+        _lib.call("vx_multi_volume_create_u8", _lib.ptr(data), *volume.dims, C.byref(self.handle),
+                  exc_type=RenderError)
+        self.devices = devices
+        self._finalizer = weakref.finalize(self, MultiVolume._release, self.handle.value)
+
+    @staticmethod
+    def _release(raw):
+        if raw:
+            try:
+                _lib.load().vx_multi_destroy(C.c_void_p(raw))
+            except Exception:
+                pass
+
+    def histogram_counts(self) -> np.ndarray:
+        out = np.zeros(256, dtype=np.uint64)
+        _lib.call("vx_multi_histogram", self.handle, _lib.ptr(out))
+        return out.astype(np.int64)
+
+
+_multi_lock = threading.Lock()
+
+
+def multi_volume(volume: Volume, devices) -> MultiVolume:
+    """The volume's replicas on ``devices``, built on first use and cached."""
+    devices = tuple(int(v) for v in devices)
+    cache = volume.__dict__.get("_vx_multi")
+    if cache is None or cache.devices != devices:
+        with _multi_lock:
+            cache = volume.__dict__.get("_vx_multi")
+            if cache is None or cache.devices != devices:
+                cache = MultiVolume(volume, devices)
+                object.__setattr__(volume, "_vx_multi", cache)
+    return cache
+
+
+def _render_multi(volume, camera, params, config, histogram, devices) -> FrameDetail:
+    mv = multi_volume(volume, devices)
+    rs, rp, fc = _native(camera, params, config, histogram, True)
+    pixels, small, pix_ptr, sp = _lib.pinned.frame(params.height, params.width)
+    out = _lib.vx_render_out()
+    out.pixels = pix_ptr
+    out.image_hist = sp
+    out.hit_count = sp + 256 * 8
+    out.samples = sp + 257 * 8
+    with _multi_lock:  # vx_init's device list is process-wide
+        _lib.call("vx_multi_render", mv.handle, C.byref(rs), C.byref(rp), C.byref(fc),
+                  C.byref(out), exc_type=RenderError)
+    return FrameDetail(pixels=pixels, hit_voxel=None, hit_t=None, hit_value=None, intensity=None,
+                       image_hist=small[:256], hit_count=int(small[256]),
+                       samples=int(small[257]))

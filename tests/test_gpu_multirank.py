@@ -243,3 +243,24 @@ def test_vx_init_multi_device_frames(vx, small_sphere_volume, small_sphere_histo
     finally:
         lib.vx_multi_destroy(m)
         _lib.call("vx_init", 1, (C.c_int * 1)(0))
+
+
+def test_render_frame_devices_kwarg(vx, small_sphere_volume, small_sphere_histogram, monkeypatch):
+    """render_frame(devices=...) (or VOXB200_DEVICES) splits the
+    frame over those GPUs from this process; the pixels, hit count and fused
+    histogram do not depend on it."""
+    cam = vx.orbit_camera(small_sphere_volume, azimuth_deg=120.0)
+    params = vx.RenderParams(width=200, height=120)
+    cfg = vx.FilterConfig(kind=vx.FilterKind.LOCAL_CLUSTER)
+    one = vx.render_frame(small_sphere_volume, cam, params, cfg, small_sphere_histogram)
+    two = vx.render_frame(small_sphere_volume, cam, params, cfg, small_sphere_histogram,
+                          devices=[0, 0])
+    assert np.array_equal(one.pixels, two.pixels) and one.hit_count == two.hit_count
+    assert np.array_equal(one.image_hist, two.image_hist)
+    monkeypatch.setenv("VOXB200_DEVICES", "0,0,0")
+    three = vx.render_frame(small_sphere_volume, cam, params, cfg, small_sphere_histogram)
+    assert np.array_equal(one.pixels, three.pixels)
+    from paper_1807_03119_b200.render import multi_volume
+
+    mv = multi_volume(small_sphere_volume, (0, 0, 0))
+    assert np.array_equal(mv.histogram_counts(), small_sphere_histogram.counts)
