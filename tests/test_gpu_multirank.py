@@ -257,8 +257,15 @@ def test_render_frame_devices_kwarg(vx, small_sphere_volume, small_sphere_histog
                           devices=[0, 0])
     assert np.array_equal(one.pixels, two.pixels) and one.hit_count == two.hit_count
     assert np.array_equal(one.image_hist, two.image_hist)
+    from paper_1807_03119_b200 import render as vxr
+
     monkeypatch.setenv("VOXB200_DEVICES", "0,0,0")
-    three = vx.render_frame(small_sphere_volume, cam, params, cfg, small_sphere_histogram)
+    vxr._env_devices.clear()  # read once per process: re-read for the test
+    try:
+        three = vx.render_frame(small_sphere_volume, cam, params, cfg, small_sphere_histogram)
+    finally:
+        monkeypatch.delenv("VOXB200_DEVICES")
+        vxr._env_devices.clear()
     assert np.array_equal(one.pixels, three.pixels)
     from paper_1807_03119_b200.render import multi_volume
 
