@@ -470,7 +470,22 @@ def render_detail(volume: Volume, camera: Camera, params: RenderParams, config: 
     out.image_hist = sp
     out.hit_count = sp + 256 * 8
     out.samples = sp + 257 * 8
-    if diagnostics:    return _finish(pixels, small, diagnostics, vox, t, val, inten)
+    if diagnostics:
+        out.diag = sp + 258 * 8
+        vox = np.empty((npx, 3), dtype=np.int32)
+        t = np.empty(npx, dtype=np.float32)
+        val = np.empty(npx, dtype=np.float64)
+        inten = np.empty(npx, dtype=np.float64)
+        out.hit_voxel = vox.ctypes.data
+        out.hit_t = t.ctypes.data
+        out.hit_value = val.ctypes.data
+        out.intensity = inten.ctypes.data
+    part = None
+    if partition is not None:
+        part = _lib.vx_partition(int(partition[0]), int(partition[1]))
+    _lib.call("vx_render", dev.handle, C.byref(rs), C.byref(rp), C.byref(fc),
+              C.byref(part) if part is not None else None, C.byref(out), exc_type=RenderError)
+    return _finish(pixels, small, diagnostics, vox, t, val, inten)
 
 
 def _finish(pixels, small, diagnostics, vox, t, val, inten) -> FrameDetail:
