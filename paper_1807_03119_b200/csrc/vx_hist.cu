@@ -28,13 +28,19 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define VX_HTMAX(k) do {} while (0)
 #endif
 
-constexpr int kHistThreads = 512;
+#ifndef VX_HIST_THREADS
+#define VX_HIST_THREADS 512
+#endif
+#ifndef VX_HIST_BLOCKS_PER_SM
+#define VX_HIST_BLOCKS_PER_SM 4
+#endif
+constexpr int kHistThreads = VX_HIST_THREADS;
 // K2 as a PDL-launched second kernel with a warm-up pass (below): measured
 // no faster than the fused last-block tail (512^3 35.8 vs 35.7 us), off
 #ifndef VX_HIST_PDL
 #define VX_HIST_PDL 0
 #endif
-constexpr int kHistBlocksPerSM = 4;
+constexpr int kHistBlocksPerSM = VX_HIST_BLOCKS_PER_SM;
 
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   uint4 r;
