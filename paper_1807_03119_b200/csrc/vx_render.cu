@@ -263,12 +263,17 @@ __device__ double pairwise_sum(const F& a, int n) {  // n <= 512
   return __dadd_rn(pw_level(a, 0, n2), pw_level(a, n2, n - n2));
 }
 
+// cluster-loop unroll of the local-cluster filter (code size vs loop overhead)
+#ifndef VX_LC_UNROLL
+#define VX_LC_UNROLL 1
+#endif
+constexpr int kLcUnroll = VX_LC_UNROLL;
 template <bool CHECKED>
 __device__ double filter_lc(const VolView& V, const FiltD& F, long long x, long long y,
                             long long z) {
   long long sum = 0;
   const int h = (F.M - 1) >> 1;
-#pragma unroll 3
+#pragma unroll kLcUnroll
   for (int c = 0; c < 9; ++c) {
     long long cx = x, cy = y, cz = z;
     if (c > 0) {
