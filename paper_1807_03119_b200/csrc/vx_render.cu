@@ -619,7 +619,7 @@ enum DiagIndex { dLookup, dInChunk, dChunkLoop, dUnused, dGroup, dFilter, dHit, 
   } while (0)
 
 constexpr int kGroup = 8;  // samples loaded together in occupied regions
-#ifndef VX_CHUNK_UNROLL
+#ifndef VX_CHUNK_UNROLL  // four-chunk trips: -1 never, 0 local cluster only, 1 every kind
 #define VX_CHUNK_UNROLL 0
 #endif
 
@@ -847,7 +847,7 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
                   g -= J * chunk;
                 }
               }
-              if (KIND == VX_FILTER_LOCAL_CLUSTER || VX_CHUNK_UNROLL)
+              if ((KIND == VX_FILTER_LOCAL_CLUSTER && VX_CHUNK_UNROLL >= 0) || VX_CHUNK_UNROLL > 0)
               while (g >= 4 * chunk && done + 3 * chunk < guard) {
                 VX_DIAG_ADD(dChunkLoop, 4);
                 base = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(base, M.adv), M.adv), M.adv), M.adv);
