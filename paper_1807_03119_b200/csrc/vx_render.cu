@@ -629,26 +629,45 @@ __device__ __forceinline__ float sample_t(float base, float s, int k) {
 }
 
 // J steps of the chunk-base recurrence base <- fl(base + adv) in closed
-// form.  Every partial sum base + i*adv (0 < i <= J, all in [base, B]) is a
-// float -- so each rounding is exact and the sequential result is B = base
-// + J*adv -- when B is a float and base and adv are both multiples of
-// ulp(B): each partial sum is then a multiple of ulp(B) >= its own ulp.  B
-// itself is exact in FP64 (24-bit operands, J < 2^20).  Returns false when
-// the condition fails (the caller steps sequentially).
+// form, one binade at a time, in integer ulps.  Inside the binade
+// [2^e, 2^(e+1)) of base every float is a multiple of u = ulp(base), so the
+// round-to-nearest sum is fl(base + adv) = base + A*u with A = adv/u rounded
+// to an integer -- independent of base unless adv/u is a tie (x.5: the
+// even-mantissa rule then reads base's last bit), which falls back.  A sum
+// reaching 2^(e+1) (mantissa carry into the exponent field) is still exact:
+// sums in [2^(e+1) - u/2, 2^(e+1) + u/2) round to 2^(e+1) on either grid.
+// So n steps add n*A to base's bit pattern while mant + n*A <= 2^23; a step
+// that would leave the binade is taken as one plain add.  Returns the steps
+// taken (< J only where it fell back: tie, adv >= ulp(base)*2^23 ... ).
 #ifndef VX_CHUNK_JUMP
-#define VX_CHUNK_JUMP 0  // measured slower (profiles/r2/r2_ab_misc.txt): off
+#define VX_CHUNK_JUMP 0  // 1: integer-ulp jumps; measured slower (profiles/r2/r2_ab_misc.txt)
 #endif
-__device__ __forceinline__ bool chunk_jump(float base, float adv, int J, float& out) {
-  const double B = __dadd_rn((double)base, __dmul_rn((double)J, (double)adv));
-  const float Bf = __double2float_rn(B);
-  if ((double)Bf != B || !(base >= 0.0f) || !(adv > 0.0f)) return false;
-  const unsigned e = (__float_as_uint(Bf) >> 23) & 0xffu;  // biased exponent of B
-  if (e < 24u || e > 253u) return false;
-  const float inv_u = __uint_as_float((277u - e) << 23);     // 2^(150 - e) = 1/ulp(B)
-  const float bs = __fmul_rn(base, inv_u), as = __fmul_rn(adv, inv_u);
-  if (bs != truncf(bs) || as != truncf(as)) return false;
-  out = Bf;
-  return true;
+__device__ __forceinline__ int chunk_jump_bits(float& base, float adv, int J) {
+  const unsigned ab = __float_as_uint(adv);
+  const int ea = (int)(ab >> 23);  // adv > 0 (normal): sign bit clear
+  const unsigned ma = (ab & 0x7fffffu) | 0x800000u;
+  unsigned b = __float_as_uint(base);
+  int n_done = 0;
+  while (n_done < J) {
+    const int eb = (int)(b >> 23);
+    const int sh = eb - ea;  // ulp(base) = 2^sh ulp(adv)
+    if (sh < 1 || sh > 23 || eb > 253 || ea < 1) break;
+    const unsigned half = 1u << (sh - 1);
+    if ((ma & (2u * half - 1u)) == half) break;  // tie
+    const unsigned A = (ma + half) >> sh;        // >= 1: ma >= 2^23 >= half
+    const unsigned room = 0x800000u - (b & 0x7fffffu);
+    unsigned n = (unsigned)(J - n_done);
+    if ((unsigned long long)n * A > room) n = room / A;
+    if (n == 0) {  // this step leaves the binade: the plain add
+      b = __float_as_uint(__fadd_rn(__uint_as_float(b), adv));
+      ++n_done;
+    } else {
+      b += n * A;
+      n_done += (int)n;
+    }
+  }
+  base = __uint_as_float(b);
+  return n_done;
 }
 
 // first index in [lo, m] whose sample t exceeds lim (m if none); O(1):
@@ -827,26 +846,21 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
               // skipped samples are non-candidates).
               const float q = __fmul_rn(__fsub_rn(lim, tk), M.inv_s);
               int g = k + (q < 2.0f ? 0 : (q > 1.0e6f ? 1000000 : (int)q - 1));
+              // whole chunks in closed form, binade by binade in integer ulps
+              // (chunk_jump_bits); what it leaves (a tie) by the sequential
+              // recurrence below
+              if (VX_CHUNK_JUMP && g >= chunk && done < guard) {
+                const int jg = g / chunk;
+                const int jd = (guard - done + chunk - 1) / chunk;
+                const int J = chunk_jump_bits(base, M.adv, jg < jd ? jg : jd);
+                VX_DIAG_ADD(dChunkLoop, J);
+                done += J * chunk;
+                g -= J * chunk;
+              }
               // four chunks per trip (same sequential recurrence, less loop
               // overhead per dependent add).  Measured per filter: local
               // cluster -1.5 % (bench frame) / -6.6 % (C4), the other kinds'
               // instantiations +2-5 % (register allocation), so LC only.
-              // whole chunks in closed form when every partial sum of the
-              // recurrence is exact (base_J = base + J*adv, see chunk_jump);
-              // otherwise (a skip crossing a binade with low bits set) the
-              // sequential recurrence below
-              if (VX_CHUNK_JUMP && g >= chunk && done < guard) {
-                const int jg = g / chunk;
-                const int jd = (guard - done + chunk - 1) / chunk;
-                const int J = jg < jd ? jg : jd;
-                float nb;
-                if (chunk_jump(base, M.adv, J, nb)) {
-                  VX_DIAG_ADD(dChunkLoop, J);
-                  base = nb;
-                  done += J * chunk;
-                  g -= J * chunk;
-                }
-              }
               if ((KIND == VX_FILTER_LOCAL_CLUSTER && VX_CHUNK_UNROLL >= 0) || VX_CHUNK_UNROLL > 0)
               while (g >= 4 * chunk && done + 3 * chunk < guard) {
                 VX_DIAG_ADD(dChunkLoop, 4);
