@@ -749,8 +749,9 @@ def run_ours(args):
         gbs = nvox / (hms * 1e-3) / 1e9
         hist_line = {"value": gbs, "unit": "GB/s", "ms": hms, "bytes": nvox,
                      "frac": gbs / peak, "peak": peak, "otsu_T": hist.otsu_threshold,
-                     "kernels": "hist_otsu_kernel (K1+K2 fused, one launch, last block runs "
-                                "Otsu), median of 10, L2 flushed"}
+                     "kernels": "hist_otsu_kernel (K1+K2 fused, one launch; an extra block "
+                                "runs Otsu once every counting block is in), median of 10, "
+                                "L2 flushed"}
         del compact
 
     # ---- roofline of the dominant kernel ----

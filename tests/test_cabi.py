@@ -110,6 +110,13 @@ def test_checked_variant_carries_the_checks():
     def sass(p):
         return subprocess.run([cob, "-sass", str(p)], capture_output=True, text=True).stdout
 
+    def with_op(text, op):  # functions whose SASS holds op
+        return {f for f, body in re.findall(r"Function : (\S+)(.*?)(?=Function :|\Z)", text, re.S)
+                if op in body}
+
     s_checked, s_prod = sass(checked), sass(_build.LIB)
     assert s_checked.count("BPT.TRAP") > 100 and "NANOSLEEP" in s_checked
-    assert "BPT.TRAP" not in s_prod and "NANOSLEEP" not in s_prod
+    assert "BPT.TRAP" not in s_prod
+    # the only sleep in production: the histogram's tail block polling the ticket
+    assert all("hist_otsu_kernel" in f for f in with_op(s_prod, "NANOSLEEP"))
+    assert with_op(s_checked, "NANOSLEEP") - with_op(s_prod, "NANOSLEEP")
