@@ -16,14 +16,17 @@
 // surface candidate when raw >= thr = ceil(T) (render.py:258,307), and only
 // an accepted candidate (f >= T) ends a ray (render.py:311-329).  Per thr
 // (and per filter setting) the volume keeps a map of 4^3 cells holding the
-// Chebyshev cell distance D (capped at 32) to the nearest cell with a
-// candidate-level voxel (the candidate map) or with an accepted voxel (the
-// accepted-cell map, K8).  At a sample in a cell with D >= skip_min_d (2 for
-// step >= 0.5, else 1), every cell within distance D-1 is empty, so every
-// later sample whose t lies before the ray's exit from that box -- its far
-// faces shrunk by 1/8 voxel, less a t margin of 1/16 + |t| 2^-19 -- truncates
-// into an empty cell (computed positions are monotone in t and their FP32
-// error is < 2^-7 voxel for |p|, |t| < 8192).  Those samples are stepped
+// Chebyshev cell distance D (capped per volume at max(dims)/16 clamped to
+// [32, 128], vx_fine_cap_for) to the nearest cell with a candidate-level
+// voxel (the candidate map) or with an accepted voxel (the accepted-cell
+// map, K8); per ray-direction orthant also a one-sided map (DESIGN.md §5:
+// only occupied cells on the side the ray moves toward count).  At a sample
+// in a cell with D >= skip_min_d (2 for step >= 0.5, else 1), every cell
+// within distance D-1 (on that side) is empty, so every later sample whose t
+// lies before the ray's exit from that box -- its far faces shrunk by 1/8
+// voxel, less a t margin of 1/16 + |t| 2^-19 -- truncates into an empty cell
+// (computed positions are monotone in t and their FP32 error is < 2^-7 voxel
+// for |p|, |t| < 8192).  Those samples are stepped
 // over by index inside a chunk and by the exact FP32 base recurrence across
 // chunks, so the t of every sample actually taken is bit-identical to the
 // reference's.  Result-neutral by construction; switched off when thr == 0
