@@ -84,13 +84,14 @@ __device__ __forceinline__ void count_vec4(uint32_t* lane_base, const uint4& a, 
   count_word(lane_base, d.z); count_word(lane_base, d.w);
 }
 
-// next != nullptr: blocks take 4*blockDim.x-vector chunks (32 KB) from the
-// counter *next (zeroed before the launch) instead of a fixed grid-stride
-// share.  Measured with %globaltimer marks: with fixed shares the first
-// block finished counting at 18.5 us and the last at 27.1 us (512^3; 136 vs
-// 187 us at 1024^3) -- SMs see unequal bandwidth -- so the kernel ended
-// with the slowest SM's share.  The next chunk's index is fetched while the
-// current chunk's loads are in flight.
+// next != nullptr: after a fixed grid-stride share of static_eighths/8 of
+// the data, blocks take 4*blockDim.x-vector chunks (32 KB) of the rest from
+// the counter *next (zeroed before the launch).  Measured with %globaltimer
+// marks: with fixed shares only, the first block finished counting at
+// 18.5 us and the last at 27.1 us (512^3; 136 vs 187 us at 1024^3) -- SMs
+// see unequal bandwidth -- so the kernel ended with the slowest SM's share.
+// The next chunk's index is fetched while the current chunk's loads are in
+// flight.  nblk: the number of counting blocks (the grid may hold one more).
 __device__ __forceinline__ void hist_block_local(const uint8_t* __restrict__ data, uint64_t n,
                                                  uint32_t* sh, uint32_t* tot,
                                                  unsigned int* next, unsigned nblk,
@@ -464,17 +465,17 @@ __global__ void __launch_bounds__(256) otsu_kernel(const unsigned long long* __r
   otsu_block(counts[threadIdx.x], S, T_out);
 }
 
-// K1+K2 in one launch (histogram.py:119-133 then :59-101).  Blocks add their
-// bins into the workspace ws[0..255]; the last block to finish (ticket in
-// ws[256]) copies them to counts_out, re-zeroes the workspace for the next
-// call on this stream, and runs the exact Otsu scan over the shared memory
-// its histogram used.  One launch, no memset: the stand-alone K1 + K2 pair
-// costs two launch gaps and a fill kernel, which is 10-20 us at 256^3-512^3.
+// K1+K2 in one launch (histogram.py:119-133 then :59-101).  Counting blocks
+// add their bins into the workspace and take a ticket; one extra block runs
+// the exact Otsu scan once every ticket is in (VX_HIST_WAITER, below; or,
+// without it, the last block to take a ticket), copies the bins to
+// counts_out and re-zeroes the workspace for the next call on this stream.
+// One launch, no memset: the stand-alone K1 + K2 pair costs two launch gaps
+// and a fill kernel, which is 10-20 us at 256^3-512^3.
 // The blocks' bin totals land in kHistRepl copies of the 256 bins (block b
-// adds into copy b % kHistRepl): ~600 blocks x 256 u64 atomics into ONE copy
-// queue up in the few L2 slices holding those 2 KB, and the tail's read of
-// the bins waits for the queue to drain (~3.5 us at 512^3, profiles/r2/
-// r2_ab_hist.txt); copies on separate lines spread that work.
+// adds into copy b % kHistRepl) to spread ~600 blocks x 256 u64 atomics over
+// more L2 lines (measured: 256^3 ~1 us faster than one copy, larger sizes
+// unchanged; profiles/r2/r2_ab_hist.txt).
 #ifndef VX_HIST_REPL
 #define VX_HIST_REPL 8
 #endif
@@ -681,7 +682,7 @@ int vx_launch_hist(const uint8_t* dev, uint64_t n, uint64_t* dev_counts, cudaStr
   return VX_OK;
 }
 
-// one zeroed workspace per (device, stream): the kernel's last block leaves
+// one zeroed workspace per (device, stream): the kernel's Otsu block leaves
 // it zeroed, and launches on one stream are ordered
 static std::mutex g_ws_mu;
 static struct WsSlot { int dev; cudaStream_t s; HistWs* p; } g_ws[64];
