@@ -70,6 +70,39 @@ def test_fused_hist_otsu_sizes(vx, oracle, n):
             assert int(T.item()) == wt
 
 
+def test_fused_hist_otsu_concurrent_streams(vx, oracle):
+    """Four streams launching K1+K2 at once, several rounds without a host
+    sync in between: each launch has its own Otsu block waiting on its own
+    counting blocks (per-stream workspaces), none waits on another's."""
+    import torch
+
+    rs = np.random.default_rng(11)
+    hosts = [rs.integers(0, 256, (1 << 24) + 7 * i, dtype=np.uint8) for i in range(4)]
+    for h in hosts:
+        h[: h.size // 3] = rs.integers(0, 40, h.size // 3, dtype=np.uint8)
+    import ctypes as C
+
+    from paper_1807_03119_b200 import _lib
+
+    devs = [torch.from_numpy(h).cuda() for h in hosts]
+    streams = [torch.cuda.Stream() for _ in hosts]
+    outs = [[(torch.full((256,), -1, dtype=torch.int64, device="cuda"),
+              torch.full((1,), -7, dtype=torch.int32, device="cuda")) for _ in hosts]
+            for _ in range(3)]
+    torch.cuda.synchronize()
+    for rnd in outs:  # launches only: no torch work between them
+        for d, s, (counts, T) in zip(devs, streams, rnd):
+            _lib.call("vx_histogram_otsu_device", C.c_void_p(d.data_ptr()), d.numel(),
+                      C.c_void_p(counts.data_ptr()), C.c_void_p(T.data_ptr()),
+                      C.c_void_p(s.cuda_stream))
+    torch.cuda.synchronize()
+    for rnd in outs:
+        for h, (counts, T) in zip(hosts, rnd):
+            want = oracle.hist256(h)
+            assert np.array_equal(counts.cpu().numpy(), want)
+            assert int(T.item()) == oracle.otsu(want)
+
+
 def test_fused_hist_otsu_goldens(vx, oracle):
     """The reference's golden Otsu histograms, expanded to bytes where small."""
     import torch
