@@ -2082,6 +2082,10 @@ static double trace_us() {
     }                                                                             \
   } while (0)
 
+#ifndef VX_ORDER_FRESH
+#define VX_ORDER_FRESH 1
+#endif
+
 // Cost dilation of the tile order for a moving camera (VOXB200_DILATE=1).
 // Measured (scripts/orbit_probe.py, 1 degree per frame): device p50 0.194
 // ms dilated vs 0.159 ms on the plain k-2 costs -- the max filter turns the
@@ -2287,6 +2291,8 @@ struct TileSched {
   int device = -1;
   vx_ray_setup last_rs[2];  // camera of the frame that recorded costs into buf[p]
   bool have_rs[2] = {false, false};
+  vx_ray_setup prev_rs;  // camera of the previous frame on this schedule
+  bool have_prev = false;
 };
 // a thread's schedules, one per (volume, frame size, partition, stream):
 // a thread alternating between frames of several kinds -- or enqueueing
@@ -2408,6 +2414,7 @@ static int tile_sched(vx_volume* vol, const vx_ray_setup* rs, int rank, int worl
       VX_CUDA(cudaMemsetAsync(t.buf[p] + grid + kSchedHdr, 0, (size_t)grid * 4, s));
       t.valid[p] = false;
       t.have_rs[p] = false;
+      t.have_prev = false;
     }
     t.vol = vol;
     t.w = rs->width;
@@ -2599,12 +2606,22 @@ static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_p
   if (ts) {
     const int p = ts->parity;
     // this frame records its costs in buf[p] and renders in the order the
-    // side stream computed there from frame k - 2 (after its order is done)
-    if (ts->valid[p]) VX_CUDA(cudaStreamWaitEvent(s, ts->order_done[p], 0));
+    // side stream computed there from frame k - 2 (after its order is done).
+    // A moving camera renders in the order of frame k - 1's costs instead
+    // (buf[p ^ 1], computed on the side stream right behind that frame): the
+    // heavy tiles move ~2 tiles per degree of orbit, and a 2-frame-old order
+    // left them unsplit and late (profiles/r2/r2_ab_misc.txt).  The wait is
+    // then on the previous frame's ordering kernel.
+    const bool moving = VX_ORDER_FRESH && ts->have_prev &&
+                        memcmp(&ts->prev_rs, rs, sizeof(vx_ray_setup)) != 0;
+    ts->prev_rs = *rs;
+    ts->have_prev = true;
+    const int q = moving && ts->valid[p ^ 1] ? p ^ 1 : p;
+    if (ts->valid[q]) VX_CUDA(cudaStreamWaitEvent(s, ts->order_done[q], 0));
     a.tile_cost = ts->buf[p] + grid + kSchedHdr;
-    a.tile_order = ts->valid[p] ? ts->buf[p] : nullptr;
-    if (ts->valid[p]) {
-      const uint32_t* dm = ts->demand[p];
+    a.tile_order = ts->valid[q] ? ts->buf[q] : nullptr;
+    if (ts->valid[q]) {
+      const uint32_t* dm = ts->demand[q];
       const long long want = 7ll * dm[0] + 3ll * dm[1] + dm[2];
       const long long reserve = want + want / 4 + 32;
       if (reserve < a.split_max) a.split_max = (int)reserve;
