@@ -10,7 +10,7 @@ boxes, slab speckle and spot noise, built only from reference primitives;
 
 from __future__ import annotations
 
-import math
+import numpy as np
 
 from . import rng
 from .volume import PhantomSpec, Shape, SpotNoise
@@ -38,25 +38,33 @@ def spot_phantom_spec(dims: int = 128, seed: int = SPOT_PHANTOM_SEED) -> Phantom
     )
 
 
+_BLOB_TAG = 0x736C6162  # the reference's substream tag for texture centres
+_BLOB_DRAWS = 10000     # draws before giving up (phantoms.py:49-68)
+
+
 def blob_positions(dims: int, count: int, sphere_radius: float, seed: int):
-    """Deterministic texture centres clear of the borders and the central sphere."""
-    c = (dims - 1) / 2.0
-    margin = 6
-    keepout = sphere_radius + 8
-    span = dims - 2 * margin
-    sub = rng.substream_seed(seed, 0x736C6162)
-    out: list[tuple[int, int, int]] = []
-    draw = 0
-    while len(out) < count and draw < 10000:
-        b = rng.stream(sub, draw * 3, 3)
-        draw += 1
-        p = (margin + int(b[0] % span), margin + int(b[1] % span), margin + int(b[2] % span))
-        if math.dist(p, (c, c, c)) < keepout:
+    """Texture centres of the reference's phantoms (phantoms.py:49-68): draw i
+    of the substream proposes the point ``6 + (draw words 3i..3i+2) mod
+    (dims - 12)``; proposals within ``sphere_radius + 8`` of the volume centre,
+    or within 10 voxels of an accepted centre, are dropped; the first
+    ``count`` survivors in draw order are the centres.
+
+    All proposals are formed at once; only the greedy spacing test runs per
+    point.  Distances are compared squared (integer points, centre on the
+    half-voxel grid: no rounding can flip a comparison)."""
+    span = dims - 12
+    words = rng.stream(rng.substream_seed(seed, _BLOB_TAG), 0, 3 * _BLOB_DRAWS)
+    pts = 6 + (words.reshape(-1, 3) % np.uint64(span)).astype(np.int64)
+    off = pts - (dims - 1) / 2.0
+    pts = pts[(off * off).sum(axis=1) >= (sphere_radius + 8) ** 2]
+    chosen = np.empty((0, 3), dtype=np.int64)
+    for p in pts:
+        if len(chosen) == count:
+            break
+        if len(chosen) and int(((chosen - p) ** 2).sum(axis=1).min()) < 100:
             continue
-        if any(math.dist(p, q) < 10 for q in out):
-            continue
-        out.append(p)
-    return out
+        chosen = np.vstack([chosen, p])
+    return [tuple(int(v) for v in p) for p in chosen]
 
 
 def speckle_phantom_spec(dims: int = 128, seed: int = SPECKLE_PHANTOM_SEED) -> PhantomSpec:

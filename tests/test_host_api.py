@@ -305,3 +305,28 @@ def test_pinned_pool_is_bounded(monkeypatch):
     assert len(pool._frames) <= pool.MAX_FRAME_SIZES
     assert pool._free_bytes <= pool.FREE_CAP
     assert freed  # the overflow went back to the driver
+
+
+def test_pgm_header_grammar(tmp_path):
+    """PGM header fields with whitespace / '#'-comment separators, one
+    whitespace byte before the payload, and the reference's error messages
+    (images.py:20-50)."""
+    from paper_1807_03119_b200.images import ImageError, read_pgm, read_pgm_header
+
+    body = bytes(range(12))
+    good = [b"P5\n4 3\n255\n", b"P5 4 3 255 ", b"P5\n# c\n4 # x\n3\n#y\n255\n",
+            b"P5#c\n4\t3\r255\x0b", b"P5\r\n4\r\n3\r\n255\r"]
+    for i, hdr in enumerate(good):
+        p = tmp_path / f"g{i}.pgm"
+        p.write_bytes(hdr + body)
+        assert read_pgm_header(p) == (4, 3, len(hdr))
+        assert read_pgm(p).tobytes() == body
+    bad = [(b"P6\n4 3\n255\n" + body, "not a binary PGM"), (b"P5\n4 3", "truncated PGM header"),
+           (b"P5\n# only a comment", "truncated PGM header"),
+           (b"P5\n4 3\n254\n" + body, "maxval must be 255, got 254"),
+           (b"P5\n4 3\n255\n" + body[:5], "payload shorter than 4x3")]
+    for i, (data, msg) in enumerate(bad):
+        p = tmp_path / f"b{i}.pgm"
+        p.write_bytes(data)
+        with pytest.raises(ImageError, match=msg):
+            read_pgm_header(p)
