@@ -1322,7 +1322,17 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kW
     block_t0 = t;
   }
   const int tile = a.rank + a.world * owned;
-  const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+  // tile / tiles_x through an FP32 reciprocal (exact for tile < 2^24 after
+  // the +-1 fix-up): a 32-bit integer division is ~25 instructions
+  int ty = __float2int_rz(__fmul_rn((float)tile, __frcp_rn((float)a.tiles_x)));
+  int tx = tile - ty * a.tiles_x;
+  if (tx < 0) {
+    --ty;
+    tx += a.tiles_x;
+  } else if (tx >= a.tiles_x) {
+    ++ty;
+    tx -= a.tiles_x;
+  }
   // the tile's 8 column u and 16 row v (one FP64 division each, render.py:
   // 193-196) once per block instead of per pixel
   __shared__ double su[kTileW], sv[kTileH];
