@@ -684,8 +684,10 @@ def run_ours(args):
                  "ms_p99": srt[min(len(srt) - 1, int(0.99 * len(srt)))], "ms_max": srt[-1],
                  "ms_first": ot[0],
                  "note": "render_frame per frame, a new Camera each frame (azimuth 45..144 deg), "
-                         "host frame out; the tile order comes from frames k-2 of the motion and "
-                         "the accepted-cell map is camera-independent (built once per setting)"}
+                         "host frame out; a moving camera renders in the tile order of frame "
+                         "k-1's costs; the accepted-cell map is camera-independent (built once "
+                         "per setting); orthant skip maps are built when the view enters a new "
+                         "direction orthant (the ms_max outlier when it happens here)"}
 
     # ---- full traversal (no skipping): the march engine on every sample ----
     noskip = None
