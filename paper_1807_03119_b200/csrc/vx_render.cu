@@ -58,6 +58,13 @@ struct RayCamD {
 #ifndef VX_RAYCAST_WPB
 #define VX_RAYCAST_WPB 4
 #endif
+// resident warps per SM the frame kernel is compiled for (64 registers at 32);
+// the no-filter and mean kinds run lighter code and gain from 40 (48
+// registers, a few spills: C2 none -3.5 %, mean -4 %; local cluster +9 %,
+// entropy +17 % there; profiles/r2/r2_ab_misc.txt)
+#ifndef VX_RAYCAST_MIN_WARPS_LIGHT
+#define VX_RAYCAST_MIN_WARPS_LIGHT 40
+#endif
 #ifndef VX_RAYCAST_MIN_WARPS
 #define VX_RAYCAST_MIN_WARPS 32
 #endif
@@ -1267,8 +1274,13 @@ __device__ unsigned g_warp_sm[1 << 20];
 __device__ unsigned g_warp_diag[9 << 20];
 #endif
 
+constexpr int raycast_min_warps(int kind) {
+  return kind == VX_FILTER_NONE || kind == VX_FILTER_MEAN ? VX_RAYCAST_MIN_WARPS_LIGHT
+                                                          : VX_RAYCAST_MIN_WARPS;
+}
+
 template <int KIND, bool CHECKED, bool DIAG, bool BUDGET, bool SKIP = true>
-__global__ void __launch_bounds__(32 * kWarpsPerBlock, VX_RAYCAST_MIN_WARPS / kWarpsPerBlock)
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, raycast_min_warps(KIND) / kWarpsPerBlock)
     raycast_kernel(const RenderArgs a) {
   __shared__ double lut[KIND == VX_FILTER_ENTROPY ? 256 : 1];
   __shared__ WarpScratch wsc[kWarpsPerBlock];
@@ -2445,6 +2457,7 @@ struct OrderJob {
   TileSched* ts = nullptr;
   int grid = 0;
   int tiles_x = 0, rx = 0, ry = 0;  // camera motion in tiles (dilation radius)
+  int min_warps = VX_RAYCAST_MIN_WARPS;  // resident warps per SM of the frame kernel
 };
 
 // Image-space motion of the volume between two cameras, in tiles: the
@@ -2495,7 +2508,7 @@ static int order_tiles(const OrderJob& j, cudaStream_t s) {
   VX_CUDA(cudaStreamWaitEvent(ts->side, ts->costs_done[p], 0));
   tile_order_kernel<<<1, 1024, 0, ts->side>>>(b + j.grid + kSchedHdr, b, j.grid,
                                               g_sched_split_us.load(),
-                                              vx_sm_count() * (VX_RAYCAST_MIN_WARPS / kWarpsPerBlock),
+                                              vx_sm_count() * (j.min_warps / kWarpsPerBlock),
                                               j.tiles_x, j.rx, j.ry,
                                               b + 2 * j.grid + kSchedHdr);
   VX_CHECK_LAUNCH();
@@ -2648,6 +2661,7 @@ static int render_impl(vx_volume* vol, const vx_ray_setup* rs, const vx_render_p
   job.ts = ts;
   job.grid = grid;
   job.tiles_x = a.tiles_x;
+  job.min_warps = raycast_min_warps(a.F.kind);
   if (ts && a.world == 1 && dilate_moving()) {
     // the order this frame's costs produce serves frame k + 2: expect the
     // camera to keep moving as it did from frame k - 2 (whose costs buf[p]
