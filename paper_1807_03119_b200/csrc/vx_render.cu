@@ -1274,9 +1274,14 @@ __device__ unsigned g_warp_sm[1 << 20];
 __device__ unsigned g_warp_diag[9 << 20];
 #endif
 
+// sigma and okada: 36 (56 registers; C2 sigma -1.5 %, okada -2.2 %)
+#ifndef VX_RAYCAST_MIN_WARPS_MID
+#define VX_RAYCAST_MIN_WARPS_MID 36
+#endif
 constexpr int raycast_min_warps(int kind) {
-  return kind == VX_FILTER_NONE || kind == VX_FILTER_MEAN ? VX_RAYCAST_MIN_WARPS_LIGHT
-                                                          : VX_RAYCAST_MIN_WARPS;
+  return kind == VX_FILTER_NONE || kind == VX_FILTER_MEAN    ? VX_RAYCAST_MIN_WARPS_LIGHT
+         : kind == VX_FILTER_SIGMA || kind == VX_FILTER_OKADA ? VX_RAYCAST_MIN_WARPS_MID
+                                                              : VX_RAYCAST_MIN_WARPS;
 }
 
 template <int KIND, bool CHECKED, bool DIAG, bool BUDGET, bool SKIP = true>
