@@ -984,8 +984,10 @@ __device__ int march(const VolView& V, const MarchD& M, const FiltD& F, const do
       // Re-measured with distance-1 cells sampled (skip_min_d 2): 4 for
       // none/mean/okada too (C1 -5 %, C2 mean -3 %, okada -1.5 %), local
       // cluster stays at 2 (4: bench +1.7 %, C2 +3.8 %, C4 +1.3 %)
+      // Late round 2, with per-kind occupancy: sigma at 2 too (C2 -3 %, C1
+      // unchanged; none / mean / okada / entropy stay at 4: C1 +5 % at 2)
       constexpr int kPipe = VX_GROUP_PIPE ? VX_GROUP_PIPE
-                            : (KIND == VX_FILTER_LOCAL_CLUSTER ? 2 : 4);
+                            : (KIND == VX_FILTER_LOCAL_CLUSTER || KIND == VX_FILTER_SIGMA ? 2 : 4);
       if (kPipe == 4) {
       for (int b = 0; b < nr; b += 16) {
         int raw0, raw1 = 0, raw2 = 0, raw3 = 0;
