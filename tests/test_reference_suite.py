@@ -38,7 +38,7 @@ DESELECT = {
         "asserts relative wall-clock timings of the reference's CPU renderer (criterion (a): "
         "'mean' is the fastest filtered mode, because CPU frame time tracks march length); "
         "its own docstring calls (a) noise-limited ('can fail honestly on busy machines'). It "
-        "passed on the B200 in the round-2 run (profiles/r2_reference_suite.txt), but a "
+        "passed on the B200 in the round-2 run (profiles/r2/r2_reference_suite.txt), but a "
         "wall-clock ordering between two sub-millisecond kernels is not a parity property",
 }
 __doc__ += "".join(f"\n* ``{k}``: {v}." for k, v in DESELECT.items())
