@@ -492,8 +492,8 @@ def test_map_cache_eviction_stress_threads(vx):
 
 def test_orbiting_camera_frames_match_oracle(vx, oracle):
     """A camera moving 3 degrees per frame: the tile order and split rays come
-    from costs of frame k-2, dilated by the camera's image-space motion;
-    whatever the schedule, every frame equals the oracle's."""
+    from the previous frame's costs (a moving camera's schedule); whatever
+    the schedule, every frame equals the oracle's."""
     from oracle.rng_np import generate_phantom_np
     from paper_1807_03119_b200 import phantoms
     from paper_1807_03119_b200.render import render_detail
